@@ -1,0 +1,183 @@
+/*
+ * sparge.h -- C ABI of the B200 (sm_100a) SpargeAttn hot path.
+ *
+ * SpargeAttn (arXiv 2502.18137) computes a two-stage block-sparse, INT8
+ * quantised attention forward pass.  Citations are PAPER.md lines (P:Lnnn)
+ * with the section / equation / Algorithm-1 line they sit in; readings of
+ * silent passages are the R# items of DESIGN.md §3.
+ *
+ * Conventions for every call:
+ *   - Pointers are DEVICE pointers unless the argument says "host".
+ *   - The caller owns every buffer.  The library never allocates or frees
+ *     device memory, never synchronises the stream (except
+ *     sparge_attn_status, which says so) and never prints.
+ *   - All work is enqueued asynchronously on `stream` (a cudaStream_t passed
+ *     as an opaque pointer; NULL = the legacy default stream).
+ *   - Tensors of tokens are [B, H, N, d] with d contiguous; `sparge_strides`
+ *     gives the element strides of the b, h and n axes.  Row starts must be
+ *     16-byte aligned (d in {64, 128}, so stride_n*2 % 16 == 0).
+ *   - Blocks: T_m = ceil(N / bq) query blocks, T_n = ceil(N / bk) key blocks
+ *     (Definition 1; reading R6).  bq = 128, bk = 64, cw = 4
+ *     are the only supported values (App. A.1).
+ *   - GQA: query head h reads key/value head h / (Hq / Hkv)  (reading R18).
+ *   - Return codes: SPARGE_OK, or SPARGE_EINVAL for argument validation
+ *     failures (nothing is enqueued), SPARGE_ECUDA for a launch error
+ *     (cudaGetLastError() holds the cause), SPARGE_ENOTIMPL for an option
+ *     that is declared but not built.  Errors are returned, never thrown.
+ */
+#ifndef SPARGE_H_
+#define SPARGE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum sparge_status {
+  SPARGE_OK = 0,
+  SPARGE_EINVAL = 2,     /* shape / stride / hyper-parameter validation      */
+  SPARGE_EINTERNAL = 3,  /* a valid query row ended with l = 0 (R8)  */
+  SPARGE_ECUDA = 4,      /* CUDA launch or driver error                      */
+  SPARGE_ENOTIMPL = 5    /* declared option not implemented in this build    */
+};
+
+enum sparge_dtype { SPARGE_BF16 = 0, SPARGE_FP16 = 1 };
+enum sparge_pv_dtype { SPARGE_PV_SAME_AS_INPUT = 0, SPARGE_PV_FP8_E4M3 = 1 };
+enum sparge_sim_mode {
+  SPARGE_SIM_COSINE = 0,   /* R1-A: mean of the row-normalised Gram matrix  */
+  SPARGE_SIM_LITERAL = 1   /* R1-B: mean(X X^T / |max(X X^T)|) on raw rows  */
+};
+
+typedef struct { int64_t b, h, n; } sparge_strides;
+
+typedef struct {
+  int B, Hq, Hkv, N, d;   /* d in {64, 128}; Hq % Hkv == 0; N >= 1          */
+  int bq, bk, cw;         /* must be 128, 64, 4                            */
+  int causal;             /* 0/1; block-causal handling per reading R8      */
+  int in_dtype;           /* enum sparge_dtype of Q, K, V, O                 */
+  int pv_dtype;           /* enum sparge_pv_dtype (FP8 -> SPARGE_ENOTIMPL)   */
+  int sim_mode;           /* enum sparge_sim_mode                           */
+  int smooth_k;           /* 0 only (R14); 1 -> SPARGE_ENOTIMPL              */
+} sparge_shape;
+
+/* Human-readable name of a status code (static string, never NULL). */
+const char* sparge_strerror(int status);
+
+/*
+ * hilbert_permute -- §3.7 "HilbertCurve Permutation" and
+ * App. A.1.  HOST call, no CUDA.
+ *
+ * Builds the generalised 3-D Hilbert order (gilbert3d, reading R19) of a
+ * T x H x W grid of visual tokens that follow `text_prefix` text tokens.
+ * Source token layout: [text_prefix text tokens][(t, h, w) row-major].
+ *   perm_host[r] = source index of position r of the permuted sequence
+ *   inv_host[s]  = position of source token s         (inv[perm[r]] = r)
+ * Both arrays have L = text_prefix + T*H*W int32 entries (host memory,
+ * caller-allocated).  Text tokens map to themselves.
+ * Errors: SPARGE_EINVAL if any extent < 1, text_prefix < 0, L > 2^31-1,
+ * or a pointer is NULL.
+ */
+int hilbert_permute(int T, int H, int W, int text_prefix,
+                    int32_t* perm_host, int32_t* inv_host);
+
+/*
+ * sparge_quantize -- Alg. 1 line 3 ("per-block quantization in
+ * SageAttention"), line 4 (block mean) and line 5 (CosSim),
+ * fused in one HBM pass.  Runs once for Q (is_key = 0, blocks of bq rows,
+ * H = Hq) and once for K (is_key = 1, blocks of bk rows, H = Hkv).
+ *
+ *   x      [B, H, N, d] in_dtype, strided by x_str (read-only)
+ *   perm   nullable int32 [N]: row r of the (permuted) sequence is x row
+ *          perm[r] (the Hilbert gather of §3.7).  NULL = identity.
+ *   xq     int8 [B, H, N, d] contiguous, permuted order: per block i,
+ *          xq = clamp(rne(fl32(x * fl32(127/amax_i))), -127, 127)  (R11)
+ *   delta  fp32 [B, H, T]: fl32(amax_i / 127); 1 for an all-zero block
+ *   pooled fp64 [B, H, T, d]: mean over the block's valid rows
+ *   sim    fp64 [B, H, T]: CosSim of the block per sim_mode     (R1)
+ * T = T_m (is_key = 0) or T_n (is_key = 1).
+ * Errors: SPARGE_EINVAL (bad shape, NULL pointer, misaligned stride),
+ * SPARGE_ENOTIMPL (smooth_k), SPARGE_ECUDA.
+ */
+int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_str,
+                    int is_key, const int32_t* perm,
+                    int8_t* xq, float* delta, double* pooled, double* sim,
+                    void* stream);
+
+/*
+ * sparge_predict_mask -- stage 1 of Algorithm 1, lines 5-6,
+ * §3.2 TopCdf and Eq. (5) fix-block forcing.
+ * Inputs are the sparge_quantize statistics of Q (per q-head) and K (per
+ * kv-head), so Q and K are read from HBM once.  fp64 (R15).
+ *
+ * For each (b, hq, i):
+ *   S^[j] = q_i . k_j / sqrt(d)                                    (R2)
+ *   S^[j] = -inf if k_sim[j] < theta, or if tile (i,j) is causally dead
+ *   P^ = softmax(S^);  keep rank k of (P^ desc, j asc) iff
+ *        cumsum_k <= tau * cumsum_last, and always rank 0          (R4)
+ *   M[i,:] = 1 if q_sim[i] < theta; M[:,j] = 1 if k_sim[j] < theta;
+ *   all -inf row -> all ones (R7); causal: M &= live, M[i, i*bq/bk] = 1 (R8)
+ * Outputs (device):
+ *   mask  nullable uint8 [B, Hq, T_m, T_n]  (M_g of Definition 1)
+ *   lut   int32 [B, Hq, T_m, T_n]: kept j of row i in ascending order
+ *   cnt   int32 [B, Hq, T_m]: number of kept j of row i (>= 1)
+ * tau in (0, 1], theta in [-1, 1] (float32, compared in fp64).
+ * Errors: SPARGE_EINVAL (range / NULL / T_n > 4096), SPARGE_ECUDA.
+ */
+int sparge_predict_mask(const sparge_shape* shape,
+                        const double* q_pooled, const double* q_sim,
+                        const double* k_pooled, const double* k_sim,
+                        float tau, float theta,
+                        uint8_t* mask, int32_t* lut, int32_t* cnt,
+                        void* stream);
+
+/* Bytes of device workspace sparge_attn_fwd needs for `shape` (V^T staging,
+ * work list, status word).  0 on invalid shape. */
+size_t sparge_attn_workspace(const sparge_shape* shape);
+
+/*
+ * sparge_attn_fwd -- stage 2 of Algorithm 1, lines 7-21:
+ * the sparse FlashAttention loop over the kept blocks with SageAttention
+ * dequantisation (line 12) and the per-warp lambda gate (lines
+ * 14-17; §3.4).
+ *
+ *   qq, dq   int8 [B, Hq, N, d] + fp32 [B, Hq, T_m]  (sparge_quantize of Q)
+ *   kq, dk   int8 [B, Hkv, N, d] + fp32 [B, Hkv, T_n] (sparge_quantize of K)
+ *   v        [B, Hkv, N, d] in_dtype, strided by v_str, ORIGINAL token order
+ *   lut, cnt from sparge_predict_mask
+ *   lambda   natural-log units of S = QK^T/sqrt(d) (R3); -INFINITY disables
+ *            the gate; must be < 0.  A warp of bq/cw rows computes its
+ *            P~V slice iff max_rows(m_local - m_new) > lambda (R5).
+ *   perm     nullable int32 [N]: the same permutation given to
+ *            sparge_quantize; V rows are gathered through it and O rows are
+ *            scattered back to original order.
+ *   o        [B, Hq, N, d] in_dtype, strided by o_str (written)
+ *   counters nullable uint64 [B, Hq, 3], ACCUMULATED (caller zeroes):
+ *            [0] executed QK tiles, [1] executed P~V warp slices,
+ *            [2] issued P~V MMAs  (sparsity per R16)
+ *   workspace/ws_bytes  >= sparge_attn_workspace(shape), 256-byte aligned;
+ *            zero-initialised once by the caller (its first word is the
+ *            status word, cleared again by sparge_attn_status)
+ * Errors: SPARGE_EINVAL, SPARGE_ENOTIMPL (pv_dtype FP8), SPARGE_ECUDA.  A
+ * row finishing with l = 0 is recorded in the workspace status word and
+ * reported by sparge_attn_status.
+ */
+int sparge_attn_fwd(const sparge_shape* shape,
+                    const int8_t* qq, const float* dq,
+                    const int8_t* kq, const float* dk,
+                    const void* v, sparge_strides v_str,
+                    const int32_t* lut, const int32_t* cnt,
+                    float lambda, const int32_t* perm,
+                    void* o, sparge_strides o_str,
+                    uint64_t* counters,
+                    void* workspace, size_t ws_bytes, void* stream);
+
+/* SYNCHRONISES `stream`, reads and clears the workspace status word:
+ * SPARGE_OK, or SPARGE_EINTERNAL if some valid row ended with l = 0. */
+int sparge_attn_status(void* workspace, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARGE_H_ */

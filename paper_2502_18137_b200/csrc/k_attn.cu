@@ -1,0 +1,428 @@
+// k_sparse_attn -- step a3 of the hot path.
+//
+// Stage 2 of Algorithm 1: for one (q-head, query block i) the
+// CTA walks the kept key blocks j of M_g (the LUT from k_predict_topcdf, in
+// ascending j) and runs the online-softmax recurrence of Eq. 1:
+//   S   = (Q^_i K^_j^T) dq_i dk_j / sqrt(d)          line 12, R3
+//   m_local = rowmax S; m_new = max(m, m_local); P~ = exp(S - m_new)
+//   l   = e^{m - m_new} l + rowsum P~                 line 13
+//   per warp w (rows 32w..32w+31, c_w = 4, R10):
+//     if max(m_local - m_new) > lambda:               line 15, R5
+//        O[I_w] = e^{m - m_new} O[I_w] + P~[I_w] V_j  line 16
+//   O_i = O / l                                       line 19
+//
+// sm_100a design (one CTA per (head, 128-row query tile), 2 CTAs per SM):
+//   warp 4    TMA producer: Q^ once, then K^_j (3-stage ring) and V^T_j
+//             (2-stage ring) for every kept j; SWIZZLE_128B/64B tiles.
+//   warp 5    MMA issuer (one thread): tcgen05.mma kind::i8 Q^K^^T -> S
+//             (int32, TMEM, double-buffered), then kind::f16 P~ V -> O
+//             (fp32, TMEM).  The P~V MMA is skipped when all four warps
+//             vote to skip (their P~ rows are zero otherwise: exact).
+//   warps 0-3 softmax: thread r owns row r == TMEM lane r.  exp2 domain
+//             (lambda compared as lambda*log2e), integer-domain row max,
+//             exact int->fp32 via the 1.5*2^23 magic constant, lazy O
+//             rescale (reference max moves only when the true max grows by
+//             > 8 in log2 units; O/l is invariant to the reference, the
+//             lambda gate always uses the true running max).
+#include <cuda.h>
+#include <cstdint>
+#include <climits>
+
+#include "sm100.cuh"
+#include "sparge_internal.h"
+
+namespace sparge {
+
+namespace {
+
+constexpr int BQ = 128;
+constexpr int BK = 64;
+constexpr int KST = 3;        // K^ stages
+constexpr int VST = 2;        // V^T stages
+constexpr int NTHREADS = 192; // 4 softmax warps + producer + MMA
+constexpr float kRescaleThreshold = 8.0f;   // log2 units
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int D>
+struct Smem {
+  static constexpr int Q_BYTES = BQ * D;        // int8
+  static constexpr int K_BYTES = BK * D;        // int8
+  static constexpr int V_BYTES = D * BK * 2;    // V^T tile, 16-bit
+  static constexpr int P_BYTES = BQ * BK * 2;   // P~ tile, 16-bit
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KST * K_BYTES;
+  static constexpr int OFF_P = OFF_V + VST * V_BYTES;
+  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 4;
+  static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;
+  static constexpr int TOTAL = OFF_MISC + 64;
+  static constexpr int ALLOC = TOTAL + 1024;     // slack for 1024-B alignment
+  static constexpr int ROW_BYTES_QK = D;          // 128 -> SW128, 64 -> SW64
+};
+
+struct AttnParams {
+  const float* dq;
+  const float* dk;
+  const int32_t* lut;
+  const int32_t* cnt;
+  const int32_t* perm;
+  uint16_t* o;
+  int64_t o_sb, o_sh, o_sn;
+  unsigned long long* counters;
+  unsigned int* status;
+  float lam2;         // lambda * log2(e)
+  float scale_log2;   // log2(e) / sqrt(d)
+  int N, T_m, T_n, Hq, Hkv, group;
+};
+
+template <int D, bool CAUSAL, bool F16>
+__global__ void __launch_bounds__(NTHREADS, 2)
+k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+              const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using L = Smem<D>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  int8_t* sQ = reinterpret_cast<int8_t*>(smem + L::OFF_Q);
+  int8_t* sK = reinterpret_cast<int8_t*>(smem + L::OFF_K);
+  unsigned char* sV = smem + L::OFF_V;
+  unsigned char* sP = smem + L::OFF_P;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + KST;
+  uint64_t* v_full = k_empty + KST;
+  uint64_t* v_empty = v_full + VST;
+  uint64_t* s_full = v_empty + VST;
+  uint64_t* s_free = s_full + 2;
+  uint64_t* p_full = s_free + 2;
+  uint64_t* o_done = p_full + 2;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  uint32_t* tmem_base_slot = misc;           // [0]
+  uint32_t* pv_flag = misc + 1;              // [2][4]
+
+  const int warp = warp_id(), lane = lane_id();
+  const int i = CAUSAL ? (p.T_m - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+  const int bhq = blockIdx.y;
+  const int b = bhq / p.Hq, hq = bhq % p.Hq;
+  const int bkv = b * p.Hkv + hq / p.group;
+  const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + i;
+  const int n_tiles = p.cnt[row_id];
+  const int32_t* lut_row = p.lut + row_id * p.T_n;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KST; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+    for (int s = 0; s < VST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(s_full + s, 1);
+      mbar_init(s_free + s, 4);
+      mbar_init(p_full + s, 4);
+      mbar_init(o_done + s, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc<256>(tmem_base_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_slot;
+  const uint32_t tS0 = tmem, tO = tmem + 128;
+
+  if (warp == 4) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      mbar_arrive_expect_tx(q_full, L::Q_BYTES);
+      tma_load_3d(sQ, &tmQ, q_full, 0, i * BQ, bhq);
+      int j_next = n_tiles > 0 ? __ldg(lut_row) : 0;
+      for (int t = 0; t < n_tiles; ++t) {
+        const int j = j_next;
+        if (t + 1 < n_tiles) j_next = __ldg(lut_row + t + 1);
+        const int ks = t % KST;
+        mbar_wait(k_empty + ks, ((t / KST) & 1) ^ 1);
+        mbar_arrive_expect_tx(k_full + ks, L::K_BYTES);
+        tma_load_3d(sK + ks * L::K_BYTES, &tmK, k_full + ks, 0, j * BK, bkv);
+        const int vs = t % VST;
+        mbar_wait(v_empty + vs, ((t / VST) & 1) ^ 1);
+        mbar_arrive_expect_tx(v_full + vs, L::V_BYTES);
+        tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
+      }
+    }
+  } else if (warp == 5) {
+    // ============================ MMA issuer ==============================
+    if (lane == 0) {
+      constexpr uint32_t IDESC_QK = idesc_i8(BQ, BK);
+      constexpr uint32_t IDESC_PV = F16 ? idesc_f16(BQ, D) : idesc_bf16(BQ, D);
+      const uint64_t dQ = umma_desc_kmajor(smem_u32(sQ), L::ROW_BYTES_QK);
+      unsigned long long issued = 0;
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto do_pv = [&](int u) {
+        const int pb = u & 1, vs = u % VST;
+        mbar_wait(p_full + pb, (u >> 1) & 1);
+        mbar_wait(v_full + vs, (u / VST) & 1);
+        tc_fence_after();
+        const bool any = (pv_flag[pb * 4 + 0] | pv_flag[pb * 4 + 1] |
+                          pv_flag[pb * 4 + 2] | pv_flag[pb * 4 + 3]) != 0;
+        if (any) {
+          const uint64_t dP = umma_desc_kmajor(smem_u32(sP + pb * L::P_BYTES), 128);
+          const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA (32 B)
+            mma_f16(tO, dP + 2 * kk, dV + 2 * kk, IDESC_PV, 1u);
+          ++issued;
+        }
+        tc_commit(v_empty + vs);
+        tc_commit(o_done + pb);
+      };
+      for (int t = 0; t < n_tiles; ++t) {
+        const int ks = t % KST, sb = t & 1;
+        mbar_wait(k_full + ks, (t / KST) & 1);
+        mbar_wait(s_free + sb, ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint64_t dK = umma_desc_kmajor(smem_u32(sK + ks * L::K_BYTES), L::ROW_BYTES_QK);
+#pragma unroll
+        for (int kk = 0; kk < D / 32; ++kk)       // K = 32 per kind::i8 MMA (32 B)
+          mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, kk > 0 ? 1u : 0u);
+        tc_commit(s_full + sb);
+        tc_commit(k_empty + ks);
+        if (t > 0) do_pv(t - 1);
+      }
+      if (n_tiles > 0) do_pv(n_tiles - 1);
+      if (p.counters) atomicAdd(p.counters + bhq * 3 + 2, issued);
+    }
+  } else {
+    // ============================ softmax warps ===========================
+    const int r = threadIdx.x;                 // row within the tile == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const int row_g = i * BQ + r;
+    const bool row_valid = row_g < p.N;
+    const bool tile_tail = (i * BQ + BQ > p.N);
+    {
+      uint32_t z[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) z[k] = 0u;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) tmem_st32(tO + lane_base + c * 32, z);
+      tmem_wait_st();
+    }
+    const float dqi = __ldg(p.dq + row_id);
+    const float* dk_row = p.dk + static_cast<int64_t>(bkv) * p.T_n;
+    float m_true = -INFINITY, m_ref = -INFINITY, l = 0.f;
+    unsigned long long slices = 0;
+    int j_next = n_tiles > 0 ? __ldg(lut_row) : 0;
+    float dk_next = n_tiles > 0 ? __ldg(dk_row + j_next) : 0.f;
+    uint32_t* prow_base = reinterpret_cast<uint32_t*>(sP) ;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int j = j_next;
+      const float c = dqi * dk_next * p.scale_log2;
+      if (t + 1 < n_tiles) {
+        j_next = __ldg(lut_row + t + 1);
+        dk_next = __ldg(dk_row + j_next);
+      }
+      const int sb = t & 1;
+      mbar_wait(s_full + sb, (t >> 1) & 1);
+      tc_fence_after();
+      int32_t a[BK];
+      tmem_ld32(tS0 + sb * BK + lane_base, reinterpret_cast<uint32_t*>(a));
+      tmem_ld32(tS0 + sb * BK + 32 + lane_base, reinterpret_cast<uint32_t*>(a) + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free + sb);
+
+      // ---- masking of boundary tiles: keys >= N, causal keys > query, rows >= N
+      const int k0 = j * BK;
+      const bool need_mask = tile_tail || (k0 + BK > p.N) || (CAUSAL && (k0 + BK - 1 > i * BQ));
+      int mx = INT_MIN;
+      if (need_mask) {
+        const int kmax = CAUSAL ? min(p.N - 1, row_g) : p.N - 1;
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+          if (!row_valid || k0 + k > kmax) a[k] = INT_MIN;
+          mx = max(mx, a[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < BK; ++k) mx = max(mx, a[k]);
+      }
+      // S = acc * dq * dk / sqrt(d), here in log2 units (x log2 e)
+      const float m_loc = (mx == INT_MIN) ? -INFINITY : static_cast<float>(mx) * c;
+      const float m_new = fmaxf(m_true, m_loc);
+      float gap = (mx == INT_MIN) ? -INFINITY : m_loc - m_new;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, o));
+      const bool compute = gap > p.lam2;        // warp-uniform (Alg. 1 line 15)
+
+      if (compute) {
+        const bool need = m_new > m_ref + kRescaleThreshold;   // true when m_ref = -inf
+        const bool rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
+        if (rescale_o) {
+          // O rows of this warp hold P~V of earlier tiles: wait for the last
+          // issued P~V, then rescale in TMEM.
+          if (t >= 1) mbar_wait(o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
+          tc_fence_after();
+          const float alpha = need ? ex2_approx(m_ref - m_new) : 1.f;
+#pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t ov[32];
+            tmem_ld32(tO + lane_base + cc * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
+            tmem_st32(tO + lane_base + cc * 32, ov);
+          }
+          tmem_wait_st();
+        }
+        if (need) {
+          l *= ex2_approx(m_ref - m_new);      // 0 when m_ref = -inf (l is 0 then)
+          m_ref = m_new;
+        }
+      }
+      m_true = m_new;
+
+      // ---- P~ = exp2(S*log2e - m_ref), row sum, bf16 tile for P~V ----
+      // int -> fp32 exactly: bits(acc + 0x4B400000) = 1.5*2^23 + acc for |acc| < 2^22
+      const float neg_ref = -m_ref;
+      const bool row_live = m_ref > -INFINITY;
+      float pv[BK];
+      float rs = 0.f;
+#pragma unroll
+      for (int k = 0; k < BK; ++k) {
+        const float s = __int_as_float(a[k] + 0x4B400000) - 12582912.0f;
+        float e = ex2_approx(fmaf(s, c, neg_ref));
+        e = (a[k] == INT_MIN || !row_live) ? 0.f : e;
+        pv[k] = e;
+        rs += e;
+      }
+      l += rs;
+
+      // P~ buffer sb was last read by P~V(t-2)
+      if (t >= 2) mbar_wait(o_done + sb, ((t - 2) >> 1) & 1);
+      uint32_t* prow = prow_base + (sb * L::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128) / 4;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        uint4 w;
+        if (compute) {
+          if (F16) {
+            w.x = pack_f16x2(pv[ch * 8 + 0], pv[ch * 8 + 1]);
+            w.y = pack_f16x2(pv[ch * 8 + 2], pv[ch * 8 + 3]);
+            w.z = pack_f16x2(pv[ch * 8 + 4], pv[ch * 8 + 5]);
+            w.w = pack_f16x2(pv[ch * 8 + 6], pv[ch * 8 + 7]);
+          } else {
+            w.x = pack_bf16x2(pv[ch * 8 + 0], pv[ch * 8 + 1]);
+            w.y = pack_bf16x2(pv[ch * 8 + 2], pv[ch * 8 + 3]);
+            w.z = pack_bf16x2(pv[ch * 8 + 4], pv[ch * 8 + 5]);
+            w.w = pack_bf16x2(pv[ch * 8 + 6], pv[ch * 8 + 7]);
+          }
+        } else {
+          w = make_uint4(0u, 0u, 0u, 0u);
+        }
+        *reinterpret_cast<uint4*>(prow + ((ch ^ (r & 7)) * 4)) = w;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        pv_flag[sb * 4 + warp] = compute ? 1u : 0u;
+        mbar_arrive(p_full + sb);
+      }
+      if (compute) ++slices;
+    }
+
+    // ---- epilogue: O_i = O / l (line 19), scattered back through perm ----
+    if (n_tiles > 0) mbar_wait(o_done + ((n_tiles - 1) & 1), ((n_tiles - 1) >> 1) & 1);
+    tc_fence_after();
+    if (row_valid && !(l > 0.f)) atomicOr(p.status, 1u);
+    const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+    const int dst_row = row_valid ? (p.perm ? __ldg(p.perm + row_g) : row_g) : 0;
+    uint16_t* orow = p.o + b * p.o_sb + hq * p.o_sh + static_cast<int64_t>(dst_row) * p.o_sn;
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t ov[32];
+      tmem_ld32(tO + lane_base + cc * 32, ov);
+      tmem_wait_ld();
+      if (row_valid) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          const float* f = reinterpret_cast<const float*>(ov) + q * 8;
+          if (F16) {
+            w.x = pack_f16x2(f[0] * inv_l, f[1] * inv_l);
+            w.y = pack_f16x2(f[2] * inv_l, f[3] * inv_l);
+            w.z = pack_f16x2(f[4] * inv_l, f[5] * inv_l);
+            w.w = pack_f16x2(f[6] * inv_l, f[7] * inv_l);
+          } else {
+            w.x = pack_bf16x2(f[0] * inv_l, f[1] * inv_l);
+            w.y = pack_bf16x2(f[2] * inv_l, f[3] * inv_l);
+            w.z = pack_bf16x2(f[4] * inv_l, f[5] * inv_l);
+            w.w = pack_bf16x2(f[6] * inv_l, f[7] * inv_l);
+          }
+          *reinterpret_cast<uint4*>(orow + cc * 32 + q * 8) = w;
+        }
+      }
+    }
+    if (p.counters) {
+      unsigned long long tot = slices;
+      if (lane == 0) atomicAdd(p.counters + bhq * 3 + 1, tot);
+      if (threadIdx.x == 0) atomicAdd(p.counters + bhq * 3 + 0, static_cast<unsigned long long>(n_tiles));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+template <int D, bool CAUSAL, bool F16>
+cudaError_t launch_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                     const AttnParams& p, int B, cudaStream_t stream) {
+  auto kern = k_sparse_attn<D, CAUSAL, F16>;
+  const int smem = Smem<D>::ALLOC;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.T_m, B * p.Hq);
+  kern<<<grid, NTHREADS, smem, stream>>>(mq, mk, mv, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
+                        const CUtensorMap& mv, const float* dq, const float* dk,
+                        const int32_t* lut, const int32_t* cnt, float lambda,
+                        const int32_t* perm, void* o, sparge_strides o_str,
+                        uint64_t* counters, unsigned int* status, cudaStream_t stream) {
+  AttnParams p;
+  p.dq = dq; p.dk = dk; p.lut = lut; p.cnt = cnt; p.perm = perm;
+  p.o = static_cast<uint16_t*>(o);
+  p.o_sb = o_str.b; p.o_sh = o_str.h; p.o_sn = o_str.n;
+  p.counters = reinterpret_cast<unsigned long long*>(counters);
+  p.status = status;
+  p.lam2 = lambda * kLog2e;     // -inf stays -inf
+  p.scale_log2 = kLog2e / sqrtf(static_cast<float>(s.d));
+  p.N = s.N;
+  p.T_m = (s.N + BQ - 1) / BQ;
+  p.T_n = (s.N + BK - 1) / BK;
+  p.Hq = s.Hq; p.Hkv = s.Hkv; p.group = s.Hq / s.Hkv;
+  const bool f16 = s.in_dtype == SPARGE_FP16;
+#define SPARGE_A(D, C, F) return launch_t<D, C, F>(mq, mk, mv, p, s.B, stream)
+  if (s.d == 128) {
+    if (s.causal) { if (f16) SPARGE_A(128, true, true); else SPARGE_A(128, true, false); }
+    else          { if (f16) SPARGE_A(128, false, true); else SPARGE_A(128, false, false); }
+  } else {
+    if (s.causal) { if (f16) SPARGE_A(64, true, true); else SPARGE_A(64, true, false); }
+    else          { if (f16) SPARGE_A(64, false, true); else SPARGE_A(64, false, false); }
+  }
+#undef SPARGE_A
+}
+
+int attn_smem_bytes(int d) { return d == 128 ? Smem<128>::ALLOC : Smem<64>::ALLOC; }
+
+}  // namespace sparge

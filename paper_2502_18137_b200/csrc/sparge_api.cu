@@ -1,0 +1,192 @@
+// C-ABI front end of libsparge (include/sparge.h): argument validation,
+// launch configuration, TMA descriptor encoding and workspace layout.  No
+// compute happens here; every step of the path runs in the kernels.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "sparge_internal.h"
+
+using namespace sparge;
+
+namespace {
+
+constexpr size_t kStatusBytes = 256;
+
+bool shape_ok(const sparge_shape* s) {
+  if (!s) return false;
+  if (s->B < 1 || s->Hq < 1 || s->Hkv < 1 || s->N < 1) return false;
+  if (s->Hq % s->Hkv) return false;
+  if (s->d != 64 && s->d != 128) return false;
+  if (s->bq != 128 || s->bk != 64 || s->cw != 4) return false;
+  if (s->causal != 0 && s->causal != 1) return false;
+  if (s->in_dtype != SPARGE_BF16 && s->in_dtype != SPARGE_FP16) return false;
+  if (s->sim_mode != SPARGE_SIM_COSINE && s->sim_mode != SPARGE_SIM_LITERAL) return false;
+  if (s->pv_dtype != SPARGE_PV_SAME_AS_INPUT && s->pv_dtype != SPARGE_PV_FP8_E4M3) return false;
+  return true;
+}
+
+bool strides_ok(sparge_strides st) {
+  // 16-bit elements, 16-byte aligned rows
+  return st.n > 0 && st.h >= 0 && st.b >= 0 && (st.n % 8) == 0 && (st.h % 8) == 0 &&
+         (st.b % 8) == 0;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int n_pad_of(const sparge_shape* s) { return ((s->N + 63) / 64) * 64; }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+bool encode3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
+              uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0,
+              uint32_t b1, CUtensorMapSwizzle sw) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  const cuuint32_t box[3] = {b0, b1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sparge_strerror(int status) {
+  switch (status) {
+    case SPARGE_OK: return "ok";
+    case SPARGE_EINVAL: return "invalid argument";
+    case SPARGE_EINTERNAL: return "internal invariant violated (a valid row ended with l = 0)";
+    case SPARGE_ECUDA: return "CUDA error";
+    case SPARGE_ENOTIMPL: return "option not implemented in this build";
+    default: return "unknown status";
+  }
+}
+
+int hilbert_permute(int T, int H, int W, int text_prefix, int32_t* perm_host,
+                    int32_t* inv_host) {
+  if (T < 1 || H < 1 || W < 1 || text_prefix < 0 || !perm_host || !inv_host)
+    return SPARGE_EINVAL;
+  const int64_t L = static_cast<int64_t>(text_prefix) + static_cast<int64_t>(T) * H * W;
+  if (L > INT32_MAX) return SPARGE_EINVAL;
+  return hilbert_build(T, H, W, text_prefix, perm_host, inv_host);
+}
+
+int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_str, int is_key,
+                    const int32_t* perm, int8_t* xq, float* delta, double* pooled, double* sim,
+                    void* stream) {
+  if (!shape_ok(shape) || !x || !xq || !delta || !pooled || !sim) return SPARGE_EINVAL;
+  if (!strides_ok(x_str) || !aligned16(x) || !aligned16(xq)) return SPARGE_EINVAL;
+  if (is_key != 0 && is_key != 1) return SPARGE_EINVAL;
+  if (shape->smooth_k) return SPARGE_ENOTIMPL;
+  cudaError_t e = launch_quant(*shape, x, x_str, is_key, perm, xq, delta, pooled, sim,
+                               static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
+}
+
+int sparge_predict_mask(const sparge_shape* shape, const double* q_pooled, const double* q_sim,
+                        const double* k_pooled, const double* k_sim, float tau, float theta,
+                        uint8_t* mask, int32_t* lut, int32_t* cnt, void* stream) {
+  if (!shape_ok(shape) || !q_pooled || !q_sim || !k_pooled || !k_sim || !lut || !cnt)
+    return SPARGE_EINVAL;
+  if (!(tau > 0.f && tau <= 1.f)) return SPARGE_EINVAL;
+  if (!(theta >= -1.f && theta <= 1.f)) return SPARGE_EINVAL;
+  const int T_n = (shape->N + shape->bk - 1) / shape->bk;
+  if (T_n > 4096) return SPARGE_EINVAL;
+  cudaError_t e = launch_predict(*shape, q_pooled, q_sim, k_pooled, k_sim, tau, theta, mask, lut,
+                                 cnt, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
+}
+
+size_t sparge_attn_workspace(const sparge_shape* shape) {
+  if (!shape_ok(shape)) return 0;
+  const size_t vt = static_cast<size_t>(shape->B) * shape->Hkv * shape->d * n_pad_of(shape) * 2;
+  return kStatusBytes + vt;
+}
+
+int sparge_attn_fwd(const sparge_shape* shape, const int8_t* qq, const float* dq,
+                    const int8_t* kq, const float* dk, const void* v, sparge_strides v_str,
+                    const int32_t* lut, const int32_t* cnt, float lambda, const int32_t* perm,
+                    void* o, sparge_strides o_str, uint64_t* counters, void* workspace,
+                    size_t ws_bytes, void* stream) {
+  if (!shape_ok(shape) || !qq || !dq || !kq || !dk || !v || !lut || !cnt || !o || !workspace)
+    return SPARGE_EINVAL;
+  if (!strides_ok(v_str) || !strides_ok(o_str) || !aligned16(v) || !aligned16(o))
+    return SPARGE_EINVAL;
+  if (!aligned16(qq) || !aligned16(kq)) return SPARGE_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return SPARGE_EINVAL;
+  if (ws_bytes < sparge_attn_workspace(shape)) return SPARGE_EINVAL;
+  if (!(lambda < 0.f)) return SPARGE_EINVAL;   // lambda < 0 or -inf (§3.6)
+  if (shape->pv_dtype != SPARGE_PV_SAME_AS_INPUT) return SPARGE_ENOTIMPL;
+  if (shape->smooth_k) return SPARGE_ENOTIMPL;
+
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const sparge_shape& s = *shape;
+  const int n_pad = n_pad_of(shape);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  unsigned int* status = reinterpret_cast<unsigned int*>(ws);
+  void* vt = ws + kStatusBytes;
+
+  cudaError_t e = launch_vprep(s, v, v_str, perm, vt, n_pad, st);
+  if (e != cudaSuccess) return SPARGE_ECUDA;
+
+  const CUtensorMapSwizzle sw_qk =
+      s.d == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  CUtensorMap mq, mk, mv;
+  const uint64_t d = static_cast<uint64_t>(s.d);
+  const uint64_t N = static_cast<uint64_t>(s.N);
+  if (!encode3d(&mq, CU_TENSOR_MAP_DATA_TYPE_UINT8, qq, d, N,
+                static_cast<uint64_t>(s.B) * s.Hq, d, d * N, s.d, 128, sw_qk) ||
+      !encode3d(&mk, CU_TENSOR_MAP_DATA_TYPE_UINT8, kq, d, N,
+                static_cast<uint64_t>(s.B) * s.Hkv, d, d * N, s.d, 64, sw_qk) ||
+      !encode3d(&mv,
+                s.in_dtype == SPARGE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                          : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                vt, static_cast<uint64_t>(n_pad), d, static_cast<uint64_t>(s.B) * s.Hkv,
+                static_cast<uint64_t>(n_pad) * 2, d * n_pad * 2, 64, s.d,
+                CU_TENSOR_MAP_SWIZZLE_128B))
+    return SPARGE_ECUDA;
+
+  e = launch_attn(s, mq, mk, mv, dq, dk, lut, cnt, lambda, perm, o, o_str, counters, status, st);
+  return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
+}
+
+int sparge_attn_status(void* workspace, void* stream) {
+  if (!workspace) return SPARGE_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned int h = 0;
+  if (cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return SPARGE_ECUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SPARGE_ECUDA;
+  if (cudaMemsetAsync(workspace, 0, sizeof(h), st) != cudaSuccess) return SPARGE_ECUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SPARGE_ECUDA;
+  return h ? SPARGE_EINTERNAL : SPARGE_OK;
+}
+
+}  // extern "C"

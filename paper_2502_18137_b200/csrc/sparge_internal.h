@@ -1,0 +1,33 @@
+// Internal declarations shared by the C-ABI front end and the kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/sparge.h"
+
+namespace sparge {
+
+cudaError_t launch_quant(const sparge_shape& s, const void* x, sparge_strides st, int is_key,
+                         const int32_t* perm, int8_t* xq, float* delta, double* pooled,
+                         double* sim, cudaStream_t stream);
+
+cudaError_t launch_predict(const sparge_shape& s, const double* q_pooled, const double* q_sim,
+                           const double* k_pooled, const double* k_sim, float tau, float theta,
+                           uint8_t* mask, int32_t* lut, int32_t* cnt, cudaStream_t stream);
+
+cudaError_t launch_vprep(const sparge_shape& s, const void* v, sparge_strides st,
+                         const int32_t* perm, void* vt, int n_pad, cudaStream_t stream);
+
+cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
+                        const CUtensorMap& mv, const float* dq, const float* dk,
+                        const int32_t* lut, const int32_t* cnt, float lambda,
+                        const int32_t* perm, void* o, sparge_strides o_str,
+                        uint64_t* counters, unsigned int* status, cudaStream_t stream);
+
+int attn_smem_bytes(int d);
+
+int hilbert_build(int T, int H, int W, int text_prefix, int32_t* perm, int32_t* inv);
+
+}  // namespace sparge

@@ -1,0 +1,167 @@
+"""Seeded synthetic workloads.  Shared by the tests, smoke()
+and bench.py for BOTH the oracle and the CUDA path; holds none of the
+method's arithmetic.
+
+All generators return float32 numpy arrays shaped [B, H, N, d]; ``to_device``
+rounds them to bf16/fp16 (RNE, via torch) -- that rounded tensor is the input
+of both sides (the oracle widens it exactly to fp64).
+
+Recipes (the structure each one plants and why):
+  planted      C1: per-block centres + noise (self-similar blocks, CosSim ~0.8)
+               with one non-self-similar Q block (i=5) and K block (j=11)
+               that are i.i.d. (CosSim ~1/n < theta) -- exercises TopCdf and
+               both forcing rules of Eq. 5.
+  llm_local    C2/C5: per kv-head AR(1) latent z_t (rho = 0.995, lag-64
+               correlation ~0.73) projected per head, plus noise; q-heads of
+               a GQA group share the latent; token 0 is an attention sink.
+               Produces local + sink attention, the Llama pattern of Fig. 2.
+  video        C3/C4: a sum of 8 random low-frequency cosines over (t, h, w)
+               projected per head, plus noise; an optional i.i.d. text
+               prefix.  Smooth neighbouring tokens (Fig. 4) so the Hilbert
+               order raises block self-similarity (§3.7).
+  gaussian     i.i.d. N(0, scale^2).
+"""
+
+import math
+
+import numpy as np
+
+__all__ = ["planted", "llm_local", "video", "gaussian", "to_device", "WORKLOADS"]
+
+
+def _rng(seed):
+    return np.random.default_rng(seed)
+
+
+def gaussian(seed, B, H, N, d, scale=1.0):
+    return (_rng(seed).standard_normal((B, H, N, d)) * scale).astype(np.float32)
+
+
+def planted(seed, N=1024, d=64, heads=1, gamma=1.5, noise=0.5, fix_q=(5,), fix_k=(11,),
+            bq=128, bk=64):
+    """C1 (BASELINE.json configs[0]): Q, K, V of shape [1, heads, N, d]."""
+    g = _rng(seed)
+    tm, tn = math.ceil(N / bq), math.ceil(N / bk)
+    q = np.empty((1, heads, N, d), np.float32)
+    k = np.empty((1, heads, N, d), np.float32)
+    for h in range(heads):
+        cq = g.standard_normal((tm, d))
+        ck = g.standard_normal((tn, d))
+        qh = np.repeat(cq, bq, axis=0)[:N] + noise * g.standard_normal((N, d))
+        kh = np.repeat(ck, bk, axis=0)[:N] + noise * g.standard_normal((N, d))
+        for i in fix_q:
+            if i < tm:
+                qh[i * bq:(i + 1) * bq] = g.standard_normal((min(bq, N - i * bq), d))
+        for j in fix_k:
+            if j < tn:
+                kh[j * bk:(j + 1) * bk] = g.standard_normal((min(bk, N - j * bk), d))
+        q[0, h] = gamma * qh
+        k[0, h] = gamma * kh
+    v = g.standard_normal((1, heads, N, d)).astype(np.float32)
+    return q, k, v
+
+
+def _ar1(g, n, width, rho):
+    """z_t = rho z_{t-1} + sqrt(1-rho^2) eps_t, stationary start."""
+    from scipy.signal import lfilter
+    eps = g.standard_normal((n, width))
+    eps[0] /= math.sqrt(1 - rho * rho)
+    return lfilter([math.sqrt(1 - rho * rho)], [1.0, -rho], eps, axis=0)
+
+
+def llm_local(seed, N, d=128, Hq=32, Hkv=8, B=1, gamma=1.2, noise=0.6, rho=0.995,
+              head_jitter=0.35, sink=4.0, heads=None):
+    """C2 / C5.  ``heads`` optionally restricts generation to a list of global
+    q-head indices (their kv-heads are generated too); every head is seeded by
+    its global index, so a subset equals the same slice of the full tensor."""
+    group = Hq // Hkv
+    hq_list = list(range(Hq)) if heads is None else list(heads)
+    kv_list = sorted({h // group for h in hq_list})
+    q = np.empty((B, len(hq_list), N, d), np.float32)
+    k = np.empty((B, len(kv_list), N, d), np.float32)
+    v = np.empty((B, len(kv_list), N, d), np.float32)
+    for b in range(B):
+        for a, g_kv in enumerate(kv_list):
+            g = _rng([seed, b, 1000 + g_kv])
+            z = _ar1(g, N, d, rho)
+            wk = g.standard_normal((d, d)) / math.sqrt(d)
+            kk = gamma * (z @ wk) + noise * g.standard_normal((N, d))
+            v[b, a] = g.standard_normal((N, d))
+            # attention sink: key 0 aligned with the group's mean query direction
+            wq_mean = np.zeros((d, d))
+            wqs = {}
+            for h in range(g_kv * group, (g_kv + 1) * group):
+                gh = _rng([seed, b, h])
+                wqs[h] = wk + head_jitter * gh.standard_normal((d, d)) / math.sqrt(d)
+                wq_mean += wqs[h] / group
+            u = (z.mean(0) @ wq_mean)
+            kk[0] = sink * math.sqrt(d) * u / (np.linalg.norm(u) + 1e-12)
+            k[b, a] = kk
+            for h in range(g_kv * group, (g_kv + 1) * group):
+                if h in hq_list:
+                    gh = _rng([seed, b, h, 7])
+                    q[b, hq_list.index(h)] = gamma * (z @ wqs[h]) + noise * gh.standard_normal((N, d))
+    return q, k, v
+
+
+def video(seed, T, H, W, d=64, heads=30, text_prefix=0, B=1, gamma=1.0, noise=0.35,
+          n_waves=8, corr_len=6.0, head_jitter=0.4, heads_subset=None):
+    """C3 / C4: tokens [text_prefix i.i.d. text][T*H*W video, (t,h,w) row-major]."""
+    n_vis = T * H * W
+    N = text_prefix + n_vis
+    hs = list(range(heads)) if heads_subset is None else list(heads_subset)
+    q = np.empty((B, len(hs), N, d), np.float32)
+    k = np.empty((B, len(hs), N, d), np.float32)
+    v = np.empty((B, len(hs), N, d), np.float32)
+    t, hh, ww = np.meshgrid(np.arange(T), np.arange(H), np.arange(W), indexing="ij")
+    coords = np.stack([t.ravel(), hh.ravel(), ww.ravel()], 1).astype(np.float64)
+    for b in range(B):
+        gb = _rng([seed, b])
+        field = np.zeros((n_vis, d))
+        for _ in range(n_waves):
+            omega = gb.standard_normal(3) / corr_len
+            phase = gb.uniform(0, 2 * math.pi)
+            field += np.cos(coords @ omega + phase)[:, None] * gb.standard_normal(d)[None, :]
+        field /= math.sqrt(n_waves / 2)
+        for a, h in enumerate(hs):
+            g = _rng([seed, b, h])
+            w = g.standard_normal((d, d)) / math.sqrt(d)
+            wq = w + head_jitter * g.standard_normal((d, d)) / math.sqrt(d)
+            wk = w + head_jitter * g.standard_normal((d, d)) / math.sqrt(d)
+            wv = g.standard_normal((d, d)) / math.sqrt(d)
+            qv = gamma * field @ wq + noise * g.standard_normal((n_vis, d))
+            kv = gamma * field @ wk + noise * g.standard_normal((n_vis, d))
+            vv = field @ wv + noise * g.standard_normal((n_vis, d))
+            txt = g.standard_normal((3, text_prefix, d))
+            q[b, a] = np.concatenate([txt[0], qv])
+            k[b, a] = np.concatenate([txt[1], kv])
+            v[b, a] = np.concatenate([txt[2], vv])
+    return q, k, v
+
+
+def to_device(x, dtype=None, device="cuda", pin=False):
+    """float32 numpy -> torch tensor rounded to bf16 (default) / fp16."""
+    import torch
+    dtype = torch.bfloat16 if dtype is None else dtype
+    t = torch.from_numpy(np.ascontiguousarray(x)).to(dtype)
+    if device == "cpu":
+        return t.pin_memory() if pin else t
+    return t.to(device)
+
+
+# name -> (generator kwargs, shape / hyper-parameters).  tau/theta/lambda are
+# BASELINE.json configs[0]'s values for every config (reading R20).
+WORKLOADS = {
+    "planted_c1": dict(kind="planted", N=1024, d=64, Hq=1, Hkv=1, causal=False),
+    "llama31_8b_32k": dict(kind="llm_local", N=32768, d=128, Hq=32, Hkv=8, causal=True),
+    "cogvideox_2b": dict(kind="video", T=13, H=30, W=45, text_prefix=226, d=64, Hq=30,
+                         Hkv=30, causal=False, hilbert=True),
+    "mochi": dict(kind="video", T=28, H=30, W=53, text_prefix=0, d=128, Hq=24, Hkv=24,
+                  causal=False, hilbert=True),
+    "sweep_8k": dict(kind="llm_local", N=8192, d=128, Hq=32, Hkv=32, causal=False),
+    "sweep_16k": dict(kind="llm_local", N=16384, d=128, Hq=32, Hkv=32, causal=False),
+    "sweep_32k": dict(kind="llm_local", N=32768, d=128, Hq=32, Hkv=32, causal=False),
+    "sweep_64k": dict(kind="llm_local", N=65536, d=128, Hq=32, Hkv=32, causal=False),
+    "sweep_128k": dict(kind="llm_local", N=131072, d=128, Hq=32, Hkv=32, causal=False),
+}
+HYPER = dict(tau=0.9, theta=0.5, lam=-5.0)

@@ -1,0 +1,182 @@
+"""Thin Python binding of libsparge.so (include/sparge.h).
+
+Argument marshalling only: every step of the SpargeAttn path runs in the
+library's CUDA kernels.  torch supplies device memory and the stream.  There
+is no CPU fallback -- importing this module without the built library raises.
+"""
+
+import ctypes
+import math
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparge.so")
+
+SPARGE_OK, SPARGE_EINVAL, SPARGE_EINTERNAL, SPARGE_ECUDA, SPARGE_ENOTIMPL = 0, 2, 3, 4, 5
+SPARGE_BF16, SPARGE_FP16 = 0, 1
+SPARGE_SIM_COSINE, SPARGE_SIM_LITERAL = 0, 1
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2502_18137_b200.build` "
+                      "(there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+
+class SpargeError(RuntimeError):
+    def __init__(self, fn, code):
+        msg = _lib.sparge_strerror(code).decode()
+        super().__init__(f"{fn} failed: {msg} ({code})")
+        self.code = code
+
+
+class Strides(ctypes.Structure):
+    _fields_ = [("b", ctypes.c_int64), ("h", ctypes.c_int64), ("n", ctypes.c_int64)]
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int) for f in
+                ("B", "Hq", "Hkv", "N", "d", "bq", "bk", "cw", "causal", "in_dtype",
+                 "pv_dtype", "sim_mode", "smooth_k")]
+
+
+_vp, _i32p, _f32p, _f64p, _u8p, _u64p, _i8p = (ctypes.c_void_p,) * 7
+_lib.sparge_strerror.restype = ctypes.c_char_p
+_lib.sparge_strerror.argtypes = [ctypes.c_int]
+_lib.hilbert_permute.restype = ctypes.c_int
+_lib.hilbert_permute.argtypes = [ctypes.c_int] * 4 + [_vp, _vp]
+_lib.sparge_quantize.restype = ctypes.c_int
+_lib.sparge_quantize.argtypes = [ctypes.POINTER(Shape), _vp, Strides, ctypes.c_int, _vp,
+                                 _vp, _vp, _vp, _vp, _vp]
+_lib.sparge_predict_mask.restype = ctypes.c_int
+_lib.sparge_predict_mask.argtypes = [ctypes.POINTER(Shape), _vp, _vp, _vp, _vp,
+                                     ctypes.c_float, ctypes.c_float, _vp, _vp, _vp, _vp]
+_lib.sparge_attn_workspace.restype = ctypes.c_size_t
+_lib.sparge_attn_workspace.argtypes = [ctypes.POINTER(Shape)]
+_lib.sparge_attn_fwd.restype = ctypes.c_int
+_lib.sparge_attn_fwd.argtypes = [ctypes.POINTER(Shape), _vp, _vp, _vp, _vp, _vp, Strides,
+                                 _vp, _vp, ctypes.c_float, _vp, _vp, Strides, _vp, _vp,
+                                 ctypes.c_size_t, _vp]
+_lib.sparge_attn_status.restype = ctypes.c_int
+_lib.sparge_attn_status.argtypes = [_vp, _vp]
+
+EXPORTED = ("sparge_strerror", "hilbert_permute", "sparge_quantize", "sparge_predict_mask",
+            "sparge_attn_workspace", "sparge_attn_fwd", "sparge_attn_status")
+
+
+def _check(fn, code):
+    if code != SPARGE_OK:
+        raise SpargeError(fn, code)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _strides(t):
+    """Element strides of the b, h, n axes of a [B, H, N, d] tensor."""
+    if t.stride(3) != 1:
+        raise ValueError("the last (d) axis must be contiguous")
+    return Strides(t.stride(0), t.stride(1), t.stride(2))
+
+
+def make_shape(B, Hq, Hkv, N, d, causal=False, dtype=torch.bfloat16, sim_mode=SPARGE_SIM_COSINE):
+    return Shape(B, Hq, Hkv, N, d, 128, 64, 4, int(bool(causal)),
+                 SPARGE_FP16 if dtype == torch.float16 else SPARGE_BF16, 0, sim_mode, 0)
+
+
+# ------------------------------------------------------------------ C-ABI calls
+def hilbert_permute(T, H, W, text_prefix=0):
+    """Host call -> (perm, inv) int32 numpy arrays (§3.7)."""
+    L = text_prefix + T * H * W
+    perm = np.empty(L, np.int32)
+    inv = np.empty(L, np.int32)
+    _check("hilbert_permute", _lib.hilbert_permute(T, H, W, text_prefix,
+                                                   perm.ctypes.data_as(ctypes.c_void_p),
+                                                   inv.ctypes.data_as(ctypes.c_void_p)))
+    return perm, inv
+
+
+def sparge_quantize(shape, x, is_key, perm, xq, delta, pooled, sim, stream=None):
+    _check("sparge_quantize", _lib.sparge_quantize(
+        ctypes.byref(shape), _ptr(x), _strides(x), int(is_key), _ptr(perm), _ptr(xq),
+        _ptr(delta), _ptr(pooled), _ptr(sim), _stream(stream)))
+
+
+def sparge_predict_mask(shape, q_pooled, q_sim, k_pooled, k_sim, tau, theta, mask, lut, cnt,
+                        stream=None):
+    _check("sparge_predict_mask", _lib.sparge_predict_mask(
+        ctypes.byref(shape), _ptr(q_pooled), _ptr(q_sim), _ptr(k_pooled), _ptr(k_sim),
+        float(tau), float(theta), _ptr(mask), _ptr(lut), _ptr(cnt), _stream(stream)))
+
+
+def sparge_attn_workspace(shape):
+    return int(_lib.sparge_attn_workspace(ctypes.byref(shape)))
+
+
+def sparge_attn_fwd(shape, qq, dq, kq, dk, v, lut, cnt, lam, perm, o, counters, workspace,
+                    stream=None):
+    _check("sparge_attn_fwd", _lib.sparge_attn_fwd(
+        ctypes.byref(shape), _ptr(qq), _ptr(dq), _ptr(kq), _ptr(dk), _ptr(v), _strides(v),
+        _ptr(lut), _ptr(cnt), float(lam), _ptr(perm), _ptr(o), _strides(o), _ptr(counters),
+        _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def sparge_attn_status(workspace, stream=None):
+    """Synchronises the stream; raises SpargeError(SPARGE_EINTERNAL) if a valid
+    row ended with l = 0."""
+    _check("sparge_attn_status", _lib.sparge_attn_status(_ptr(workspace), _stream(stream)))
+
+
+# ------------------------------------------------------------------ plumbing
+class Buffers:
+    """Device buffers of one forward pass, allocated once with torch."""
+
+    def __init__(self, shape, device="cuda", with_mask=True):
+        B, Hq, Hkv, N, d = shape.B, shape.Hq, shape.Hkv, shape.N, shape.d
+        tm, tn = math.ceil(N / 128), math.ceil(N / 64)
+        kw = dict(device=device)
+        self.shape = shape
+        self.qq = torch.empty(B, Hq, N, d, dtype=torch.int8, **kw)
+        self.kq = torch.empty(B, Hkv, N, d, dtype=torch.int8, **kw)
+        self.dq = torch.empty(B, Hq, tm, dtype=torch.float32, **kw)
+        self.dk = torch.empty(B, Hkv, tn, dtype=torch.float32, **kw)
+        self.q_pooled = torch.empty(B, Hq, tm, d, dtype=torch.float64, **kw)
+        self.k_pooled = torch.empty(B, Hkv, tn, d, dtype=torch.float64, **kw)
+        self.q_sim = torch.empty(B, Hq, tm, dtype=torch.float64, **kw)
+        self.k_sim = torch.empty(B, Hkv, tn, dtype=torch.float64, **kw)
+        self.mask = torch.empty(B, Hq, tm, tn, dtype=torch.uint8, **kw) if with_mask else None
+        self.lut = torch.empty(B, Hq, tm, tn, dtype=torch.int32, **kw)
+        self.cnt = torch.empty(B, Hq, tm, dtype=torch.int32, **kw)
+        self.counters = torch.zeros(B, Hq, 3, dtype=torch.int64, **kw)
+        ws = sparge_attn_workspace(shape)
+        self.workspace = torch.zeros((ws + 255) // 256 * 256, dtype=torch.uint8, **kw)
+
+
+def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=None, out=None,
+                   sim_mode=SPARGE_SIM_COSINE, stream=None):
+    """The whole hot path (a1 quantise Q, K -> a2 predict -> a3 attention) on
+    device tensors q [B,Hq,N,d], k/v [B,Hkv,N,d] (bf16 or fp16).  perm: optional
+    int32 device tensor [N] (Hilbert order); O is returned in original order.
+    Returns (O, buffers)."""
+    B, Hq, N, d = q.shape
+    Hkv = k.shape[1]
+    shape = make_shape(B, Hq, Hkv, N, d, causal, q.dtype, sim_mode)
+    if buffers is None:
+        buffers = Buffers(shape, device=q.device)
+    bf = buffers
+    o = torch.empty_like(q) if out is None else out
+    sparge_quantize(shape, q, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim, stream)
+    sparge_quantize(shape, k, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim, stream)
+    sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, tau, theta,
+                        bf.mask, bf.lut, bf.cnt, stream)
+    sparge_attn_fwd(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm, o,
+                    bf.counters, bf.workspace, stream)
+    return o, bf
