@@ -1,0 +1,476 @@
+#!/usr/bin/env python
+"""SpargeAttn hot-path benchmark (contract: DESIGN.md §7).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
+
+One step = the whole hot path on one batch element of the
+workload: a1 quantise Q and K (+ pool + CosSim), a2 predict the block mask,
+a3 stage V^T and run the sparse attention kernel.  The metric is the paper's
+speed 1/t = O(attn)/t in TOPS, with O(attn) the dense attention op
+count (4 N^2 d H, causal: 4 d H N(N+1)/2, reading R8-v) and t the device time
+of the step (prediction included).
+
+Multi-GPU (torchrun): every rank runs its own batch element (seeded by rank)
+with no data-path collective -> "scaling": "weak"; value = all ranks' dense
+ops / max-over-ranks step time.  Inputs are synthetic (paper_2502_18137_b200
+.inputs); the oracle (oracle/) is used only for the cpu_baseline leg, the
+sampled parity figures and --impl reference.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "effective attention TOPS & sparsity at seq 8K–128K vs dense; L1 err vs oracle"
+LOG2E = 1.4426950408889634
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="llama31_8b_32k")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="minimal run for ncu: warmup + steps only, no side legs")
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload
+def workload_cfg(name):
+    from paper_2502_18137_b200 import inputs
+    cfg = dict(inputs.WORKLOADS[name])
+    cfg.update(inputs.HYPER)
+    if cfg["kind"] == "video":
+        cfg["N"] = cfg["text_prefix"] + cfg["T"] * cfg["H"] * cfg["W"]
+    return cfg
+
+
+def gen_inputs(cfg, seed, heads=None):
+    """float32 numpy [1, H, N, d] arrays + optional Hilbert perm (numpy int32)."""
+    from paper_2502_18137_b200 import inputs
+    perm = None
+    if cfg["kind"] == "llm_local":
+        q, k, v = inputs.llm_local(seed, cfg["N"], d=cfg["d"], Hq=cfg["Hq"], Hkv=cfg["Hkv"],
+                                   heads=heads)
+    elif cfg["kind"] == "video":
+        q, k, v = inputs.video(seed, cfg["T"], cfg["H"], cfg["W"], d=cfg["d"], heads=cfg["Hq"],
+                               text_prefix=cfg["text_prefix"], heads_subset=heads)
+    else:
+        q, k, v = inputs.planted(seed, N=cfg["N"], d=cfg["d"], heads=cfg["Hq"])
+    return q, k, v
+
+
+def hilbert_perm(cfg):
+    if not cfg.get("hilbert"):
+        return None
+    from paper_2502_18137_b200 import sparge
+    perm, _ = sparge.hilbert_permute(cfg["T"], cfg["H"], cfg["W"], cfg["text_prefix"])
+    return perm
+
+
+def dense_ops(cfg, B=1):
+    N, d, H = cfg["N"], cfg["d"], cfg["Hq"]
+    if cfg["causal"]:
+        return 4.0 * d * H * B * N * (N + 1) / 2.0
+    return 4.0 * d * H * B * N * N
+
+
+def sample_qblocks(tm, seed=0):
+    rng = np.random.default_rng(seed)
+    base = {0, 1, tm // 2, tm - 1}
+    extra = rng.choice(tm, size=min(4, tm), replace=False).tolist()
+    return sorted(b for b in base.union(extra) if 0 <= b < tm)
+
+
+def sample_dense_ops(cfg, qblocks):
+    N, d = cfg["N"], cfg["d"]
+    ops = 0.0
+    for i in qblocks:
+        for r in range(i * 128, min((i + 1) * 128, N)):
+            ops += 4.0 * d * ((r + 1) if cfg["causal"] else N)
+    return ops
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu_id), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.2)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2502_18137_b200 import inputs, sparge
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = workload_cfg(args.workload)
+    N, d, Hq, Hkv = cfg["N"], cfg["d"], cfg["Hq"], cfg["Hkv"]
+    tau, theta, lam = cfg["tau"], cfg["theta"], cfg["lam"]
+
+    qn, kn, vn = gen_inputs(cfg, seed=1000 + rank)
+    perm_np = hilbert_perm(cfg)
+    qh, kh, vh = (inputs.to_device(a, device="cpu", pin=True) for a in (qn, kn, vn))
+    q, k, v = (t.to(dev) for t in (qh, kh, vh))
+    perm = None if perm_np is None else torch.from_numpy(perm_np).to(dev)
+    shape = sparge.make_shape(1, Hq, Hkv, N, d, cfg["causal"], q.dtype)
+    bf = sparge.Buffers(shape, device=dev)
+    o = torch.empty_like(q)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None, counters=bf.counters, t=tau, th=theta, lm=lam, q_=q, k_=k, v_=v, o_=o):
+        if ev: ev[0].record()
+        sparge.sparge_quantize(shape, q_, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim)
+        sparge.sparge_quantize(shape, k_, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim)
+        if ev: ev[1].record()
+        sparge.sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, t, th,
+                                   bf.mask, bf.lut, bf.cnt)
+        if ev: ev[2].record()
+        sparge.sparge_attn_fwd_ex(shape, bf.qq, bf.dq, bf.kq, bf.dk, v_, bf.lut, bf.cnt, lm, perm,
+                                  o_, counters, bf.workspace, sparge.SPARGE_ATTN_VPREP_ONLY)
+        if ev: ev[3].record()
+        sparge.sparge_attn_fwd_ex(shape, bf.qq, bf.dq, bf.kq, bf.dk, v_, bf.lut, bf.cnt, lm, perm,
+                                  o_, counters, bf.workspace, sparge.SPARGE_ATTN_SKIP_VPREP)
+        if ev: ev[4].record()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # one untimed step for sparsity / counters / parity samples
+    bf.counters.zero_()
+    step()
+    sparge.sparge_attn_status(bf.workspace)
+    cnt0 = bf.counters.cpu().numpy().astype(np.int64)
+    snap = (o[0, 0].float().cpu(), bf.mask[0, 0].cpu())   # head 0 for the parity leg
+    qk_exec, pv_slices, pv_mma = (int(cnt0[0, :, c].sum()) for c in range(3))
+    tm, tn = math.ceil(N / 128), math.ceil(N / 64)
+    if cfg["causal"]:
+        live = sum(min(tn, (min((i + 1) * 128, N) - 1) // 64 + 1) for i in range(tm)) * Hq
+    else:
+        live = tm * tn * Hq
+    sparsity = 1.0 - (qk_exec + pv_slices / 4.0) / (2.0 * live)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    gpu_id = torch.cuda.get_device_properties(dev).uuid
+    gpu_id = f"GPU-{gpu_id}" if not str(gpu_id).startswith("GPU-") else str(gpu_id)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(gpu_id) as clk:
+        for s in range(K):
+            flush.zero_()                      # L2 flush between steps (not timed)
+            step(evs[s])
+        torch.cuda.synchronize()
+    barrier()
+    st = np.array([[evs[s][a].elapsed_time(evs[s][a + 1]) for a in range(4)] for s in range(K)])
+    step_ms = st.sum(1)
+    ms = max_over_ranks(float(step_ms.mean()))
+    stages = dict(zip(["quant_ms", "predict_ms", "vprep_ms", "attn_ms"], st.mean(0).tolist()))
+    ops_rank = dense_ops(cfg)
+    value = ops_rank * world / (ms * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (k_sparse_attn) ----
+    per_tile_qk = 2.0 * 128 * 64 * d
+    per_slice_pv = 2.0 * 32 * 64 * d
+    ops_qk = qk_exec * per_tile_qk
+    ops_pv = pv_slices * per_slice_pv
+    attn_s = stages["attn_ms"] * 1e-3
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        bf16_peak, peak_src = float(peaks["bf16_tflops"]), "measured"
+    except Exception:
+        bf16_peak, peak_src = 1590.0, "fallback"
+    i8_peak = 2.0 * bf16_peak          # INT8 dense = 2x bf16 (nominal ratio, 4.5 vs 2.25 POPS)
+    mix_peak = (ops_qk + ops_pv) / (ops_qk / i8_peak + ops_pv / bf16_peak)
+    achieved = (ops_qk + ops_pv) / attn_s / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.workload)
+    roofline = {"bound": "tensor", "kernel": "k_sparse_attn", "achieved": achieved,
+                "peak": mix_peak, "unit": "TFLOP/s", "frac": achieved / mix_peak,
+                "traffic": traffic,
+                "peak_note": f"INT8 QK at 2x bf16 {peak_src} ({i8_peak:.0f}) + bf16 PV "
+                             f"({bf16_peak:.0f}), weighted by the executed op mix"}
+
+    result = {
+        "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8+bf16", "data": "synthetic",
+        "config": {"workload": args.workload, "B_per_gpu": 1, "global_batch": world, "N": N,
+                   "d": d, "Hq": Hq, "Hkv": Hkv, "causal": bool(cfg["causal"]),
+                   "hilbert": bool(cfg.get("hilbert")), "tau": tau, "theta": theta,
+                   "lambda": lam, "parallelism": f"batch x{world} (independent, no collective)",
+                   "l2": "flushed (512 MB write) between timed steps"},
+        "sparsity": sparsity,
+        "counters": {"qk_tiles": qk_exec, "pv_warp_slices": pv_slices, "pv_mmas": pv_mma,
+                     "live_tiles": live},
+        "stages_ms": stages,
+        "roofline": roofline,
+        "gpu_launches": 5 * K,
+        "clocks": clk.summary(),
+    }
+    if args.profile:
+        emit(result, rank, args)
+        return
+
+    # ---- dense comparator: same kernels, all-ones mask, lambda = -inf ----
+    if not args.no_dense:
+        Kd = min(K, 10)
+        evd = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(Kd)]
+        step(counters=None, t=1.0, th=-1.0, lm=-math.inf)
+        torch.cuda.synchronize()
+        for s in range(Kd):
+            flush.zero_()
+            step(evd[s], counters=None, t=1.0, th=-1.0, lm=-math.inf)
+        torch.cuda.synchronize()
+        dms = max_over_ranks(float(np.mean([evd[s][0].elapsed_time(evd[s][4]) for s in range(Kd)])))
+        dense_value = ops_rank * world / (dms * 1e-3) / 1e12
+        result["dense"] = {"value": dense_value, "ms_per_step": dms,
+                           "speedup": dense_value and value / dense_value,
+                           "target_0.8/(1-s)": 0.8 / max(1e-9, 1.0 - sparsity)}
+
+    # ---- e2e through the public API with host buffers ----
+    if not args.no_e2e:
+        oh = torch.empty_like(qh, device="cpu").pin_memory()
+        Ke = min(K, 10)
+        eve = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(Ke)]
+        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+        def e2e_step():
+            qd.copy_(qh, non_blocking=True)
+            kd.copy_(kh, non_blocking=True)
+            vd.copy_(vh, non_blocking=True)
+            sparge.sparge_forward(qd, kd, vd, tau, theta, lam, causal=cfg["causal"], perm=perm,
+                                  buffers=bf, out=o)
+            oh.copy_(o, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        for s in range(Ke):
+            eve[s][0].record()
+            e2e_step()
+            eve[s][1].record()
+        torch.cuda.synchronize()
+        ems = max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in eve])))
+        result["e2e"] = {"value": ops_rank * world / (ems * 1e-3) / 1e12, "unit": "TOPS",
+                         "ms_per_step": ems,
+                         "h2d_bytes_per_step": int(sum(t.numel() * t.element_size()
+                                                       for t in (qh, kh, vh))),
+                         "d2h_bytes_per_step": int(oh.numel() * oh.element_size())}
+
+    # ---- cpu_baseline + sampled parity (rank 0, N=1 only) ----
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result.update(cpu_leg(cfg, q, k, v, snap, perm_np))
+    emit(result, rank, args)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info()]
+        return max(n) if n else 1
+    except Exception:
+        return 1
+
+
+def cpu_leg(cfg, q, k, v, snap, perm_np):
+    """Time the oracle as it stands on this host on a bounded sample of the
+    same workload (q-head 0: full stage-1 prediction + the sparse loop on
+    sampled query blocks) and compare the GPU's mask / O with it."""
+    import oracle as O
+    N, d = cfg["N"], cfg["d"]
+    tm = math.ceil(N / 128)
+    group = cfg["Hq"] // cfg["Hkv"]
+    qs = q[0, 0].float().cpu().double().numpy()
+    ks = k[0, 0].float().cpu().double().numpy()
+    vs = v[0, 0].float().cpu().double().numpy()
+    if perm_np is not None:
+        qs, ks, vs = qs[perm_np], ks[perm_np], vs[perm_np]
+    qb = sample_qblocks(tm)
+    t0 = time.perf_counter()
+    o_ref, M, near, cnt, _ = O.spargeattn_head(qs, ks, vs, O.f32(cfg["tau"]), O.f32(cfg["theta"]),
+                                               O.f32(cfg["lam"]), causal=cfg["causal"],
+                                               qblocks=qb)
+    secs = time.perf_counter() - t0
+    rows = np.concatenate([np.arange(i * 128, min((i + 1) * 128, N)) for i in qb])
+    og = snap[0].double().numpy()
+    if perm_np is not None:
+        og = og[perm_np]                  # GPU O back to permuted order
+    l1 = float(np.abs(og[rows] - o_ref[rows]).sum() / np.abs(o_ref[rows]).sum())
+    dense_rows = O.dense_attention(qs, ks, vs, causal=cfg["causal"], rows=rows)
+    l1_dense = float(np.abs(og[rows] - dense_rows).sum() / np.abs(dense_rows).sum())
+    gm = snap[1].numpy()
+    mism = gm != M
+    ops = sample_dense_ops(cfg, qb)
+    _ = group
+    return {
+        "cpu_baseline": {"value": ops / secs / 1e12, "unit": "TOPS", "cores": oracle_threads(),
+                         "kind": "oracle", "seconds": secs,
+                         "sample": f"q-head 0: full stage-1 prediction + sparse loop on "
+                                   f"q-blocks {qb} ({len(rows)} of {N} rows)"},
+        "parity": {"l1_vs_oracle": l1, "l1_vs_dense": l1_dense,
+                   "mask_mismatch": int(mism.sum()),
+                   "mask_mismatch_outside_near": int((mism & ~near).sum()),
+                   "near_threshold": int(near.sum()), "head": 0, "rows": int(len(rows))},
+    }
+
+
+def emit(result, rank, args):
+    if rank != 0:
+        return
+    line = json.dumps(result)
+    print(line, flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(line + "\n")
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The oracle as it stands on the host cores (the tier's reference arm).
+    Under torchrun only rank 0 runs; the others exit 0 without work."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    cfg = workload_cfg(args.workload)
+    N, d = cfg["N"], cfg["d"]
+    tm = math.ceil(N / 128)
+    qn, kn, vn = gen_inputs(cfg, seed=1000, heads=[0])
+    import torch
+    qs, ks, vs = (torch.from_numpy(a[0, 0]).bfloat16().double().numpy() for a in (qn, kn, vn))
+    perm = hilbert_perm(cfg)
+    if perm is not None:
+        qs, ks, vs = qs[perm], ks[perm], vs[perm]
+    rng = np.random.default_rng(0)
+    times, ops = [], []
+    for s in range(args.warmup + args.steps):
+        qb = sorted(rng.choice(tm, size=min(2, tm), replace=False).tolist())
+        t0 = time.perf_counter()
+        O.spargeattn_head(qs, ks, vs, O.f32(cfg["tau"]), O.f32(cfg["theta"]), O.f32(cfg["lam"]),
+                          causal=cfg["causal"], qblocks=qb)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            ops.append(sample_dense_ops(cfg, qb))
+    value = sum(ops) / sum(times) / 1e12
+    ms = 1e3 * sum(times) / len(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "N": N, "d": d, "Hq": cfg["Hq"],
+                   "Hkv": cfg["Hkv"], "causal": bool(cfg["causal"]), "tau": cfg["tau"],
+                   "theta": cfg["theta"], "lambda": cfg["lam"]},
+        "cpu_baseline": {"value": value, "unit": "TOPS", "cores": oracle_threads(),
+                         "kind": "oracle",
+                         "sample": "per step: q-head 0 full stage-1 prediction + sparse loop "
+                                   "on 2 random q-blocks"},
+        "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

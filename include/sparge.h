@@ -173,6 +173,26 @@ int sparge_attn_fwd(const sparge_shape* shape,
                     uint64_t* counters,
                     void* workspace, size_t ws_bytes, void* stream);
 
+/* sparge_attn_fwd split into its two launches, for per-kernel timing:
+ *   flags = 0                          same as sparge_attn_fwd
+ *   flags = SPARGE_ATTN_VPREP_ONLY     only stage V^T (+ Hilbert gather) into
+ *                                      the workspace
+ *   flags = SPARGE_ATTN_SKIP_VPREP     only the attention kernel; V^T must
+ *                                      already be in the workspace from a
+ *                                      VPREP_ONLY call with the same v/perm
+ * Same arguments, validation and errors as sparge_attn_fwd. */
+enum { SPARGE_ATTN_VPREP_ONLY = 1, SPARGE_ATTN_SKIP_VPREP = 2 };
+int sparge_attn_fwd_ex(const sparge_shape* shape,
+                       const int8_t* qq, const float* dq,
+                       const int8_t* kq, const float* dk,
+                       const void* v, sparge_strides v_str,
+                       const int32_t* lut, const int32_t* cnt,
+                       float lambda, const int32_t* perm,
+                       void* o, sparge_strides o_str,
+                       uint64_t* counters,
+                       void* workspace, size_t ws_bytes, void* stream,
+                       unsigned flags);
+
 /* SYNCHRONISES `stream`, reads and clears the workspace status word:
  * SPARGE_OK, or SPARGE_EINTERNAL if some valid row ended with l = 0. */
 int sparge_attn_status(void* workspace, void* stream);

@@ -171,13 +171,25 @@ k_predict_topcdf(const double* __restrict__ q_pooled, const double* __restrict__
     for (int k = k0; k < k1; ++k) loc += s_key[k];
     double csum_total;
     const double off = block_excl_scan(loc, s_wd, &csum_total);
-    // c_last: the last element of the cumulative sum (R4)
-    const double thr = tau * csum_total;
     double c = off;
     for (int k = k0; k < k1; ++k) {
       c += s_key[k];
-      s_flag[s_idx[k]] = (c <= thr || k == 0) ? 1 : 0;
+      s_key[k] = c;
     }
+    // c_last, the last element of the cumulative sum (R4).  In exact
+    // arithmetic the cumsum is monotone and c_last is its maximum; taking the
+    // maximum of the computed values keeps "tau = 1 keeps every rank" exact
+    // when the parallel scan's rounding makes the sequence non-monotone by
+    // an ulp.
+    double cmax = (k1 > k0) ? c : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    if (lane == 0) s_wd[wid] = cmax;
+    __syncthreads();
+    cmax = s_wd[0];
+    for (int w = 1; w < kWarps; ++w) cmax = fmax(cmax, s_wd[w]);
+    const double thr = tau * cmax;
+    for (int k = k0; k < k1; ++k) s_flag[s_idx[k]] = (s_key[k] <= thr || k == 0) ? 1 : 0;
     __syncthreads();
   }
 

@@ -135,6 +135,16 @@ int sparge_attn_fwd(const sparge_shape* shape, const int8_t* qq, const float* dq
                     const int32_t* lut, const int32_t* cnt, float lambda, const int32_t* perm,
                     void* o, sparge_strides o_str, uint64_t* counters, void* workspace,
                     size_t ws_bytes, void* stream) {
+  return sparge_attn_fwd_ex(shape, qq, dq, kq, dk, v, v_str, lut, cnt, lambda, perm, o, o_str,
+                            counters, workspace, ws_bytes, stream, 0u);
+}
+
+int sparge_attn_fwd_ex(const sparge_shape* shape, const int8_t* qq, const float* dq,
+                       const int8_t* kq, const float* dk, const void* v, sparge_strides v_str,
+                       const int32_t* lut, const int32_t* cnt, float lambda,
+                       const int32_t* perm, void* o, sparge_strides o_str, uint64_t* counters,
+                       void* workspace, size_t ws_bytes, void* stream, unsigned flags) {
+  if (flags > 2u) return SPARGE_EINVAL;
   if (!shape_ok(shape) || !qq || !dq || !kq || !dk || !v || !lut || !cnt || !o || !workspace)
     return SPARGE_EINVAL;
   if (!strides_ok(v_str) || !strides_ok(o_str) || !aligned16(v) || !aligned16(o))
@@ -153,8 +163,12 @@ int sparge_attn_fwd(const sparge_shape* shape, const int8_t* qq, const float* dq
   unsigned int* status = reinterpret_cast<unsigned int*>(ws);
   void* vt = ws + kStatusBytes;
 
-  cudaError_t e = launch_vprep(s, v, v_str, perm, vt, n_pad, st);
-  if (e != cudaSuccess) return SPARGE_ECUDA;
+  cudaError_t e = cudaSuccess;
+  if (!(flags & SPARGE_ATTN_SKIP_VPREP)) {
+    e = launch_vprep(s, v, v_str, perm, vt, n_pad, st);
+    if (e != cudaSuccess) return SPARGE_ECUDA;
+  }
+  if (flags & SPARGE_ATTN_VPREP_ONLY) return SPARGE_OK;
 
   const CUtensorMapSwizzle sw_qk =
       s.d == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;

@@ -59,11 +59,15 @@ _lib.sparge_attn_fwd.restype = ctypes.c_int
 _lib.sparge_attn_fwd.argtypes = [ctypes.POINTER(Shape), _vp, _vp, _vp, _vp, _vp, Strides,
                                  _vp, _vp, ctypes.c_float, _vp, _vp, Strides, _vp, _vp,
                                  ctypes.c_size_t, _vp]
+_lib.sparge_attn_fwd_ex.restype = ctypes.c_int
+_lib.sparge_attn_fwd_ex.argtypes = _lib.sparge_attn_fwd.argtypes + [ctypes.c_uint]
 _lib.sparge_attn_status.restype = ctypes.c_int
 _lib.sparge_attn_status.argtypes = [_vp, _vp]
 
 EXPORTED = ("sparge_strerror", "hilbert_permute", "sparge_quantize", "sparge_predict_mask",
-            "sparge_attn_workspace", "sparge_attn_fwd", "sparge_attn_status")
+            "sparge_attn_workspace", "sparge_attn_fwd", "sparge_attn_fwd_ex",
+            "sparge_attn_status")
+SPARGE_ATTN_VPREP_ONLY, SPARGE_ATTN_SKIP_VPREP = 1, 2
 
 
 def _check(fn, code):
@@ -127,6 +131,15 @@ def sparge_attn_fwd(shape, qq, dq, kq, dk, v, lut, cnt, lam, perm, o, counters, 
         ctypes.byref(shape), _ptr(qq), _ptr(dq), _ptr(kq), _ptr(dk), _ptr(v), _strides(v),
         _ptr(lut), _ptr(cnt), float(lam), _ptr(perm), _ptr(o), _strides(o), _ptr(counters),
         _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def sparge_attn_fwd_ex(shape, qq, dq, kq, dk, v, lut, cnt, lam, perm, o, counters, workspace,
+                       flags, stream=None):
+    _check("sparge_attn_fwd_ex", _lib.sparge_attn_fwd_ex(
+        ctypes.byref(shape), _ptr(qq), _ptr(dq), _ptr(kq), _ptr(dk), _ptr(v), _strides(v),
+        _ptr(lut), _ptr(cnt), float(lam), _ptr(perm), _ptr(o), _strides(o), _ptr(counters),
+        _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream),
+        int(flags)))
 
 
 def sparge_attn_status(workspace, stream=None):
