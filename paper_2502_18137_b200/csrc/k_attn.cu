@@ -214,16 +214,27 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     const float* dk_row = p.dk + static_cast<int64_t>(bkv) * p.T_n;
     float m_true = -INFINITY, m_ref = -INFINITY, l = 0.f;
     unsigned long long slices = 0;
-    int j_next = n_tiles > 0 ? __ldg(lut_row) : 0;
-    float dk_next = n_tiles > 0 ? __ldg(dk_row + j_next) : 0.f;
-    uint32_t* prow_base = reinterpret_cast<uint32_t*>(sP) ;
+    // The kept j and their dk are cached per warp 32 tiles at a time (lane u
+    // holds tile 32*chunk + u) and broadcast with shuffles, so no global load
+    // sits on the per-tile critical path.  The next chunk's j is loaded at
+    // t%32 == 0 and its dk at t%32 == 16 (by then j has arrived).
+    int cj = 0, nj = 0;
+    float cdk = 0.f, ndk = 0.f;
+    if (lane < n_tiles) {
+      cj = __ldg(lut_row + lane);
+      cdk = __ldg(dk_row + cj);
+    }
+    uint32_t* prow_base = reinterpret_cast<uint32_t*>(sP);
     for (int t = 0; t < n_tiles; ++t) {
-      const int j = j_next;
-      const float c = dqi * dk_next * p.scale_log2;
-      if (t + 1 < n_tiles) {
-        j_next = __ldg(lut_row + t + 1);
-        dk_next = __ldg(dk_row + j_next);
+      const int tl = t & 31;
+      if (tl == 0) {
+        if (t > 0) { cj = nj; cdk = ndk; }
+        if (t + 32 + lane < n_tiles) nj = __ldg(lut_row + t + 32 + lane);
+      } else if (tl == 16) {
+        if (t + 16 + lane < n_tiles) ndk = __ldg(dk_row + nj);
       }
+      const int j = __shfl_sync(0xffffffffu, cj, tl);
+      const float c = dqi * __shfl_sync(0xffffffffu, cdk, tl) * p.scale_log2;
       const int sb = t & 1;
       mbar_wait(s_full + sb, (t >> 1) & 1);
       tc_fence_after();
@@ -238,18 +249,23 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       // ---- masking of boundary tiles: keys >= N, causal keys > query, rows >= N
       const int k0 = j * BK;
       const bool need_mask = tile_tail || (k0 + BK > p.N) || (CAUSAL && (k0 + BK - 1 > i * BQ));
-      int mx = INT_MIN;
       if (need_mask) {
         const int kmax = CAUSAL ? min(p.N - 1, row_g) : p.N - 1;
 #pragma unroll
-        for (int k = 0; k < BK; ++k) {
+        for (int k = 0; k < BK; ++k)
           if (!row_valid || k0 + k > kmax) a[k] = INT_MIN;
-          mx = max(mx, a[k]);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < BK; ++k) mx = max(mx, a[k]);
       }
+      // integer-domain row max (monotone: the dequant scale c > 0), four
+      // independent chains
+      int m4[4] = {a[0], a[1], a[2], a[3]};
+#pragma unroll
+      for (int k = 4; k < BK; k += 4) {
+        m4[0] = max(m4[0], a[k]);
+        m4[1] = max(m4[1], a[k + 1]);
+        m4[2] = max(m4[2], a[k + 2]);
+        m4[3] = max(m4[3], a[k + 3]);
+      }
+      const int mx = max(max(m4[0], m4[1]), max(m4[2], m4[3]));
       // S = acc * dq * dk / sqrt(d), here in log2 units (x log2 e)
       const float m_loc = (mx == INT_MIN) ? -INFINITY : static_cast<float>(mx) * c;
       const float m_new = fmaxf(m_true, m_loc);
@@ -288,18 +304,30 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       // ---- P~ = exp2(S*log2e - m_ref), row sum, bf16 tile for P~V ----
       // int -> fp32 exactly: bits(acc + 0x4B400000) = 1.5*2^23 + acc for |acc| < 2^22
       const float neg_ref = -m_ref;
-      const bool row_live = m_ref > -INFINITY;
       float pv[BK];
-      float rs = 0.f;
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+      if (need_mask) {
+        // boundary tile: masked entries (and rows with no valid key yet) give 0
+        const bool row_live = m_ref > -INFINITY;
 #pragma unroll
-      for (int k = 0; k < BK; ++k) {
-        const float s = __int_as_float(a[k] + 0x4B400000) - 12582912.0f;
-        float e = ex2_approx(fmaf(s, c, neg_ref));
-        e = (a[k] == INT_MIN || !row_live) ? 0.f : e;
-        pv[k] = e;
-        rs += e;
+        for (int k = 0; k < BK; ++k) {
+          const float s = __int_as_float(a[k] + 0x4B400000) - 12582912.0f;
+          float e = ex2_approx(fmaf(s, c, neg_ref));
+          e = (a[k] == INT_MIN || !row_live) ? 0.f : e;
+          pv[k] = e;
+          rs4[k & 3] += e;
+        }
+      } else {
+        // interior tile: every key valid and m_ref finite for every valid row
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+          const float s = __int_as_float(a[k] + 0x4B400000) - 12582912.0f;
+          const float e = ex2_approx(fmaf(s, c, neg_ref));
+          pv[k] = e;
+          rs4[k & 3] += e;
+        }
       }
-      l += rs;
+      l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
 
       // P~ buffer sb was last read by P~V(t-2)
       if (t >= 2) mbar_wait(o_done + sb, ((t - 2) >> 1) & 1);

@@ -26,14 +26,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// Block until the phase with parity `parity` of `bar` has completed.
+// Block until the phase with parity `parity` of `bar` has completed.  The
+// suspend-time hint lets the waiting warp sleep in hardware instead of
+// re-issuing try_wait (spinning warps steal issue slots from the softmax).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}"
-      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+      ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u) : "memory");
 }
 
 // ------------------------------------------------------------------ TMA

@@ -11,8 +11,8 @@ Recipes (the structure each one plants and why):
                with one non-self-similar Q block (i=5) and K block (j=11)
                that are i.i.d. (CosSim ~1/n < theta) -- exercises TopCdf and
                both forcing rules of Eq. 5.
-  llm_local    C2/C5: per kv-head AR(1) latent z_t (rho = 0.995, lag-64
-               correlation ~0.73) projected per head, plus noise; q-heads of
+  llm_local    C2/C5: per kv-head AR(1) latent z_t (rho = 0.998, lag-64
+               correlation ~0.88) projected per head, plus noise; q-heads of
                a GQA group share the latent; token 0 is an attention sink.
                Produces local + sink attention, the Llama pattern of Fig. 2.
   video        C3/C4: a sum of 8 random low-frequency cosines over (t, h, w)
@@ -69,8 +69,8 @@ def _ar1(g, n, width, rho):
     return lfilter([math.sqrt(1 - rho * rho)], [1.0, -rho], eps, axis=0)
 
 
-def llm_local(seed, N, d=128, Hq=32, Hkv=8, B=1, gamma=1.2, noise=0.6, rho=0.995,
-              head_jitter=0.35, sink=4.0, heads=None):
+def llm_local(seed, N, d=128, Hq=32, Hkv=8, B=1, gamma=0.7, noise=0.6, rho=0.998,
+              head_jitter=0.35, sink=1.0, v_noise=0.5, heads=None):
     """C2 / C5.  ``heads`` optionally restricts generation to a list of global
     q-head indices (their kv-heads are generated too); every head is seeded by
     its global index, so a subset equals the same slice of the full tensor."""
@@ -86,7 +86,8 @@ def llm_local(seed, N, d=128, Hq=32, Hkv=8, B=1, gamma=1.2, noise=0.6, rho=0.995
             z = _ar1(g, N, d, rho)
             wk = g.standard_normal((d, d)) / math.sqrt(d)
             kk = gamma * (z @ wk) + noise * g.standard_normal((N, d))
-            v[b, a] = g.standard_normal((N, d))
+            wv = g.standard_normal((d, d)) / math.sqrt(d)
+            v[b, a] = z @ wv + v_noise * g.standard_normal((N, d))
             # attention sink: key 0 aligned with the group's mean query direction
             wq_mean = np.zeros((d, d))
             wqs = {}

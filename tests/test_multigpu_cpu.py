@@ -1,0 +1,97 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): shard arithmetic and the
+property that sharded execution gathered back equals the single-process
+result bit for bit (the shards are independent; any difference is a bug).
+The per-head compute here is the oracle (the GPU kernels need a B200)."""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2502_18137_b200.shard import shard_batch, shard_heads, static_efficiency
+
+
+def test_shard_heads_cover_and_keep_groups():
+    for Hq, Hkv in [(32, 8), (30, 30), (24, 24), (32, 32), (8, 2)]:
+        for world in (1, 2, 4, 8):
+            seen = []
+            for r in range(world):
+                q0, q1, kv0, kv1 = shard_heads(Hq, Hkv, world, r)
+                assert q1 - q0 == (kv1 - kv0) * (Hq // Hkv)
+                seen.extend(range(q0, q1))
+                for h in range(q0, q1):
+                    assert kv0 <= h // (Hq // Hkv) < kv1
+            assert seen == list(range(Hq))
+
+
+def test_static_efficiency_matches_survey():
+    """C3's 30 heads -> 8/8/7/7 at 4 ranks (93.75 %)."""
+    assert [shard_heads(30, 30, 4, r)[1] - shard_heads(30, 30, 4, r)[0] for r in range(4)] == \
+        [8, 8, 7, 7]
+    assert static_efficiency(30, 4) == pytest.approx(30 / 4 / 8)
+    assert static_efficiency(8, 8) == 1.0
+
+
+def test_shard_batch():
+    for B in (1, 2, 7, 8):
+        for world in (1, 2, 4):
+            got = [shard_batch(B, world, r) for r in range(world)]
+            assert got[0][0] == 0 and got[-1][1] == B
+            assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q, k, v, out_path):
+    import oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    Hq, Hkv = q.shape[0], k.shape[0]
+    q0, q1, kv0, kv1 = shard_heads(Hq, Hkv, world, rank)
+    group = Hq // Hkv
+    mine = np.stack([O.spargeattn_head(q[h], k[h // group], v[h // group], 0.9, 0.5, -5.0,
+                                       causal=True)[0] for h in range(q0, q1)])
+    t = torch.from_numpy(mine)
+    sizes = [shard_heads(Hq, Hkv, world, r)[1] - shard_heads(Hq, Hkv, world, r)[0]
+             for r in range(world)]
+    bufs = [torch.empty((s,) + tuple(t.shape[1:]), dtype=t.dtype) for s in sizes]
+    # gloo all_gather needs equal shapes: pad to the largest shard
+    mx = max(sizes)
+    pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype)
+    pad[: t.shape[0]] = t
+    gathered = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(gathered, pad)
+    # the max-over-ranks timing reduction bench.py uses
+    tm = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        full = torch.cat([g[:s] for g, s in zip(gathered, sizes)]).numpy()
+        np.save(out_path, full)
+        assert tm.item() == world
+    dist.destroy_process_group()
+
+
+def test_head_sharded_gather_equals_single_process(tmp_path):
+    g = np.random.default_rng(0)
+    Hq, Hkv, N, d = 4, 2, 300, 32
+    q = g.standard_normal((Hq, N, d))
+    k = g.standard_normal((Hkv, N, d))
+    v = g.standard_normal((Hkv, N, d))
+    out = str(tmp_path / "o.npy")
+    mp.spawn(_worker, args=(2, _free_port(), q, k, v, out), nprocs=2, join=True)
+    got = np.load(out)
+    import oracle as O
+    ref = np.stack([O.spargeattn_head(q[h], k[h // 2], v[h // 2], 0.9, 0.5, -5.0,
+                                      causal=True)[0] for h in range(Hq)])
+    assert np.array_equal(got, ref)
