@@ -11,19 +11,23 @@
 //        O[I_w] = e^{m - m_new} O[I_w] + P~[I_w] V_j  line 16
 //   O_i = O / l                                       line 19
 //
-// sm_100a design (one CTA per (head, 128-row query tile), 2 CTAs per SM):
-//   warp 4    TMA producer: Q^ once, then K^_j (3-stage ring) and V^T_j
-//             (2-stage ring) for every kept j; SWIZZLE_128B/64B tiles.
-//   warp 5    MMA issuer (one thread): tcgen05.mma kind::i8 Q^K^^T -> S
-//             (int32, TMEM, double-buffered), then kind::f16 P~ V -> O
-//             (fp32, TMEM).  The P~V MMA is skipped when all four warps
-//             vote to skip (their P~ rows are zero otherwise: exact).
+// sm_100a design (one CTA per (head, 128-row query tile), 2 CTAs per SM,
+// 256 TMEM columns each: S0 | S1 (int32, 64 cols each) | O (fp32, d cols)):
+//   warp 4    TMA producer: Q^ once, then K^_j (4-stage ring) and V^T_j
+//             (3-stage ring) for every kept j; SWIZZLE_128B/64B tiles.
+//   warp 5    MMA issuer (one thread): tcgen05.mma kind::i8 Q^K^^T -> S[t%2]
+//             then kind::f16 P~ V -> O with P~ read from TMEM (TS form).
+//             The P~V MMA is skipped when all four warps vote to skip
+//             (their P~ rows are zero otherwise: exact).
 //   warps 0-3 softmax: thread r owns row r == TMEM lane r.  exp2 domain
-//             (lambda compared as lambda*log2e), integer-domain row max,
-//             exact int->fp32 via the 1.5*2^23 magic constant, lazy O
-//             rescale (reference max moves only when the true max grows by
-//             > 8 in log2 units; O/l is invariant to the reference, the
-//             lambda gate always uses the true running max).
+//             (lambda compared as lambda*log2e); the gate max is a warp vote
+//             (max_r gap_r > lambda  <=>  any_r gap_r > lambda); integer
+//             row max; exact int->fp32 via the 1.5*2^23 magic constant;
+//             packed f32x2 arithmetic; P~ (bf16) written back into the first
+//             32 columns of its own S buffer; lazy O rescale (R22: the
+//             reference max moves only when the true max grows by > 8 in log2
+//             units; O/l is invariant to the reference, the gate always uses
+//             the true running max).
 #include <cuda.h>
 #include <cstdint>
 #include <climits>
@@ -37,24 +41,24 @@ namespace {
 
 constexpr int BQ = 128;
 constexpr int BK = 64;
-constexpr int KST = 3;        // K^ stages
-constexpr int VST = 2;        // V^T stages
+constexpr int KST = 4;        // K^ stages
+constexpr int VST = 3;        // V^T stages
 constexpr int NTHREADS = 192; // 4 softmax warps + producer + MMA
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kMagic = 0x4B400000;          // bits of 1.5 * 2^23
+constexpr float kMagicF = 12582912.0f;
 
 template <int D>
 struct Smem {
   static constexpr int Q_BYTES = BQ * D;        // int8
   static constexpr int K_BYTES = BK * D;        // int8
   static constexpr int V_BYTES = D * BK * 2;    // V^T tile, 16-bit
-  static constexpr int P_BYTES = BQ * BK * 2;   // P~ tile, 16-bit
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * K_BYTES;
-  static constexpr int OFF_P = OFF_V + VST * V_BYTES;
-  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 4;
+  static constexpr int OFF_BAR = OFF_V + VST * V_BYTES;
+  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 3;
   static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;
   static constexpr int TOTAL = OFF_MISC + 64;
   static constexpr int ALLOC = TOTAL + 1024;     // slack for 1024-B alignment
@@ -76,6 +80,38 @@ struct AttnParams {
   int N, T_m, T_n, Hq, Hkv, group;
 };
 
+// ---- packed f32x2 helpers (FADD2 / FFMA2 on sm_100a) ----
+__device__ __forceinline__ uint64_t pk(float lo, float hi) {
+  return (static_cast<uint64_t>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <bool F16>
+__device__ __forceinline__ uint32_t pack16(float lo, float hi) {
+  return F16 ? pack_f16x2(lo, hi) : pack_bf16x2(lo, hi);
+}
+
 template <int D, bool CAUSAL, bool F16>
 __global__ void __launch_bounds__(NTHREADS, 2)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -87,7 +123,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   int8_t* sQ = reinterpret_cast<int8_t*>(smem + L::OFF_Q);
   int8_t* sK = reinterpret_cast<int8_t*>(smem + L::OFF_K);
   unsigned char* sV = smem + L::OFF_V;
-  unsigned char* sP = smem + L::OFF_P;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
@@ -95,8 +130,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   uint64_t* v_full = k_empty + KST;
   uint64_t* v_empty = v_full + VST;
   uint64_t* s_full = v_empty + VST;
-  uint64_t* s_free = s_full + 2;
-  uint64_t* p_full = s_free + 2;
+  uint64_t* p_full = s_full + 2;
   uint64_t* o_done = p_full + 2;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   uint32_t* tmem_base_slot = misc;           // [0]
@@ -117,7 +151,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     for (int s = 0; s < VST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
     for (int s = 0; s < 2; ++s) {
       mbar_init(s_full + s, 1);
-      mbar_init(s_free + s, 4);
       mbar_init(p_full + s, 4);
       mbar_init(o_done + s, 1);
     }
@@ -169,11 +202,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         const bool any = (pv_flag[pb * 4 + 0] | pv_flag[pb * 4 + 1] |
                           pv_flag[pb * 4 + 2] | pv_flag[pb * 4 + 3]) != 0;
         if (any) {
-          const uint64_t dP = umma_desc_kmajor(smem_u32(sP + pb * L::P_BYTES), 128);
           const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
+          const uint32_t tP = tS0 + pb * BK;     // P~ bf16, 32 packed columns
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA (32 B)
-            mma_f16(tO, dP + 2 * kk, dV + 2 * kk, IDESC_PV, 1u);
+          for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
+            mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
           ++issued;
         }
         tc_commit(v_empty + vs);
@@ -182,7 +215,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       for (int t = 0; t < n_tiles; ++t) {
         const int ks = t % KST, sb = t & 1;
         mbar_wait(k_full + ks, (t / KST) & 1);
-        mbar_wait(s_free + sb, ((t >> 1) & 1) ^ 1);
+        // S[sb] holds P~(t-2) until P~V(t-2) has read it
+        if (t >= 2) mbar_wait(o_done + sb, ((t - 2) >> 1) & 1);
         tc_fence_after();
         const uint64_t dK = umma_desc_kmajor(smem_u32(sK + ks * L::K_BYTES), L::ROW_BYTES_QK);
 #pragma unroll
@@ -224,7 +258,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       cj = __ldg(lut_row + lane);
       cdk = __ldg(dk_row + cj);
     }
-    uint32_t* prow_base = reinterpret_cast<uint32_t*>(sP);
     for (int t = 0; t < n_tiles; ++t) {
       const int tl = t & 31;
       if (tl == 0) {
@@ -236,15 +269,14 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       const int j = __shfl_sync(0xffffffffu, cj, tl);
       const float c = dqi * __shfl_sync(0xffffffffu, cdk, tl) * p.scale_log2;
       const int sb = t & 1;
+      const uint32_t tS = tS0 + sb * BK + lane_base;
+
       mbar_wait(s_full + sb, (t >> 1) & 1);
       tc_fence_after();
       int32_t a[BK];
-      tmem_ld32(tS0 + sb * BK + lane_base, reinterpret_cast<uint32_t*>(a));
-      tmem_ld32(tS0 + sb * BK + 32 + lane_base, reinterpret_cast<uint32_t*>(a) + 32);
+      tmem_ld32(tS, reinterpret_cast<uint32_t*>(a));
+      tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(a) + 32);
       tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_free + sb);
 
       // ---- masking of boundary tiles: keys >= N, causal keys > query, rows >= N
       const int k0 = j * BK;
@@ -255,8 +287,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         for (int k = 0; k < BK; ++k)
           if (!row_valid || k0 + k > kmax) a[k] = INT_MIN;
       }
-      // integer-domain row max (monotone: the dequant scale c > 0), four
-      // independent chains
+      // integer-domain row max (monotone: the dequant scale c > 0)
       int m4[4] = {a[0], a[1], a[2], a[3]};
 #pragma unroll
       for (int k = 4; k < BK; k += 4) {
@@ -269,10 +300,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       // S = acc * dq * dk / sqrt(d), here in log2 units (x log2 e)
       const float m_loc = (mx == INT_MIN) ? -INFINITY : static_cast<float>(mx) * c;
       const float m_new = fmaxf(m_true, m_loc);
-      float gap = (mx == INT_MIN) ? -INFINITY : m_loc - m_new;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, o));
-      const bool compute = gap > p.lam2;        // warp-uniform (Alg. 1 line 15)
+      // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
+      const bool lane_gt = (mx != INT_MIN) && (m_loc - m_new > p.lam2);
+      const bool compute = __any_sync(0xffffffffu, lane_gt);
 
       if (compute) {
         const bool need = m_new > m_ref + kRescaleThreshold;   // true when m_ref = -inf
@@ -301,58 +331,47 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       }
       m_true = m_new;
 
-      // ---- P~ = exp2(S*log2e - m_ref), row sum, bf16 tile for P~V ----
+      // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ into TMEM ----
       // int -> fp32 exactly: bits(acc + 0x4B400000) = 1.5*2^23 + acc for |acc| < 2^22
-      const float neg_ref = -m_ref;
-      float pv[BK];
-      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint64_t neg_magic2 = pk(-kMagicF, -kMagicF);
+      const uint64_t c2 = pk(c, c);
+      const uint64_t nref2 = pk(-m_ref, -m_ref);
+      uint64_t rs2[2] = {0ull, 0ull};
+      uint32_t pw[BK / 2];
       if (need_mask) {
         // boundary tile: masked entries (and rows with no valid key yet) give 0
         const bool row_live = m_ref > -INFINITY;
 #pragma unroll
-        for (int k = 0; k < BK; ++k) {
-          const float s = __int_as_float(a[k] + 0x4B400000) - 12582912.0f;
-          float e = ex2_approx(fmaf(s, c, neg_ref));
-          e = (a[k] == INT_MIN || !row_live) ? 0.f : e;
-          pv[k] = e;
-          rs4[k & 3] += e;
+        for (int k = 0; k < BK; k += 2) {
+          const uint64_t s2 = add2(pk(__int_as_float(a[k] + kMagic), __int_as_float(a[k + 1] + kMagic)),
+                                   neg_magic2);
+          const uint64_t x2 = fma2(s2, c2, nref2);
+          float e0 = ex2_approx(lo_f(x2)), e1 = ex2_approx(hi_f(x2));
+          e0 = (a[k] == INT_MIN || !row_live) ? 0.f : e0;
+          e1 = (a[k + 1] == INT_MIN || !row_live) ? 0.f : e1;
+          rs2[(k >> 1) & 1] = add2(rs2[(k >> 1) & 1], pk(e0, e1));
+          pw[k >> 1] = compute ? pack16<F16>(e0, e1) : 0u;
         }
       } else {
         // interior tile: every key valid and m_ref finite for every valid row
 #pragma unroll
-        for (int k = 0; k < BK; ++k) {
-          const float s = __int_as_float(a[k] + 0x4B400000) - 12582912.0f;
-          const float e = ex2_approx(fmaf(s, c, neg_ref));
-          pv[k] = e;
-          rs4[k & 3] += e;
+        for (int k = 0; k < BK; k += 2) {
+          const uint64_t s2 = add2(pk(__int_as_float(a[k] + kMagic), __int_as_float(a[k + 1] + kMagic)),
+                                   neg_magic2);
+          const uint64_t x2 = fma2(s2, c2, nref2);
+          const float e0 = ex2_approx(lo_f(x2)), e1 = ex2_approx(hi_f(x2));
+          rs2[(k >> 1) & 1] = add2(rs2[(k >> 1) & 1], pk(e0, e1));
+          pw[k >> 1] = compute ? pack16<F16>(e0, e1) : 0u;
         }
       }
-      l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+      const uint64_t rs = add2(rs2[0], rs2[1]);
+      l += lo_f(rs) + hi_f(rs);
 
-      // P~ buffer sb was last read by P~V(t-2)
-      if (t >= 2) mbar_wait(o_done + sb, ((t - 2) >> 1) & 1);
-      uint32_t* prow = prow_base + (sb * L::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128) / 4;
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        uint4 w;
-        if (compute) {
-          if (F16) {
-            w.x = pack_f16x2(pv[ch * 8 + 0], pv[ch * 8 + 1]);
-            w.y = pack_f16x2(pv[ch * 8 + 2], pv[ch * 8 + 3]);
-            w.z = pack_f16x2(pv[ch * 8 + 4], pv[ch * 8 + 5]);
-            w.w = pack_f16x2(pv[ch * 8 + 6], pv[ch * 8 + 7]);
-          } else {
-            w.x = pack_bf16x2(pv[ch * 8 + 0], pv[ch * 8 + 1]);
-            w.y = pack_bf16x2(pv[ch * 8 + 2], pv[ch * 8 + 3]);
-            w.z = pack_bf16x2(pv[ch * 8 + 4], pv[ch * 8 + 5]);
-            w.w = pack_bf16x2(pv[ch * 8 + 6], pv[ch * 8 + 7]);
-          }
-        } else {
-          w = make_uint4(0u, 0u, 0u, 0u);
-        }
-        *reinterpret_cast<uint4*>(prow + ((ch ^ (r & 7)) * 4)) = w;
-      }
-      fence_proxy_async_smem();
+      // P~(t) overwrites the first 32 columns of S[sb]: S(t) is already in
+      // registers and P~V(t-2), the last reader of this buffer, completed
+      // before the MMA warp issued QK(t).
+      tmem_st32(tS, pw);
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -379,17 +398,10 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         for (int q = 0; q < 4; ++q) {
           uint4 w;
           const float* f = reinterpret_cast<const float*>(ov) + q * 8;
-          if (F16) {
-            w.x = pack_f16x2(f[0] * inv_l, f[1] * inv_l);
-            w.y = pack_f16x2(f[2] * inv_l, f[3] * inv_l);
-            w.z = pack_f16x2(f[4] * inv_l, f[5] * inv_l);
-            w.w = pack_f16x2(f[6] * inv_l, f[7] * inv_l);
-          } else {
-            w.x = pack_bf16x2(f[0] * inv_l, f[1] * inv_l);
-            w.y = pack_bf16x2(f[2] * inv_l, f[3] * inv_l);
-            w.z = pack_bf16x2(f[4] * inv_l, f[5] * inv_l);
-            w.w = pack_bf16x2(f[6] * inv_l, f[7] * inv_l);
-          }
+          w.x = pack16<F16>(f[0] * inv_l, f[1] * inv_l);
+          w.y = pack16<F16>(f[2] * inv_l, f[3] * inv_l);
+          w.z = pack16<F16>(f[4] * inv_l, f[5] * inv_l);
+          w.w = pack16<F16>(f[6] * inv_l, f[7] * inv_l);
           *reinterpret_cast<uint4*>(orow + cc * 32 + q * 8) = w;
         }
       }
@@ -403,6 +415,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   tc_fence_before();
   __syncthreads();
   if (warp == 5) {
+    __syncwarp();
     tc_fence_after();
     tmem_dealloc<256>(tmem);
   }
