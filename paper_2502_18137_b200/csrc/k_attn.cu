@@ -215,8 +215,10 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       for (int t = 0; t < n_tiles; ++t) {
         const int ks = t % KST, sb = t & 1;
         mbar_wait(k_full + ks, (t / KST) & 1);
-        // S[sb] holds P~(t-2) until P~V(t-2) has read it
-        if (t >= 2) mbar_wait(o_done + sb, ((t - 2) >> 1) & 1);
+        // S[sb] holds P~(t-2), read by P~V(t-2), which this thread issued
+        // before this QK(t): tcgen05.mma from one thread execute in issue
+        // order, so no completion wait is needed (the softmax warps finished
+        // reading S(t-2) before they arrived on p_full(t-2)).
         tc_fence_after();
         const uint64_t dK = umma_desc_kmajor(smem_u32(sK + ks * L::K_BYTES), L::ROW_BYTES_QK);
 #pragma unroll
@@ -368,14 +370,15 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       l += lo_f(rs) + hi_f(rs);
 
       // P~(t) overwrites the first 32 columns of S[sb]: S(t) is already in
-      // registers and P~V(t-2), the last reader of this buffer, completed
-      // before the MMA warp issued QK(t).
+      // registers, and QK(t) -- complete, per s_full -- executed after
+      // P~V(t-2), the previous reader of this buffer.
       tmem_st32(tS, pw);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        pv_flag[sb * 4 + warp] = compute ? 1u : 0u;
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + warp)),
+                     "r"(compute ? 1u : 0u) : "memory");
         mbar_arrive(p_full + sb);
       }
       if (compute) ++slices;
