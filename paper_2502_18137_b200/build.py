@@ -32,8 +32,16 @@ def _needs(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False):
+def build(verbose=False, force=False, defines=(), lib=None):
+    """Compile csrc/ into `lib` (default libsparge.so).  `defines` adds -D
+    flags (e.g. SPARGE_PHASE_TIMING for the instrumented debug library,
+    built into its own object directory and .so)."""
+    global BUILD, LIB
+    if defines:
+        BUILD = os.path.join(HERE, "_build_" + "_".join(d.lower() for d in defines))
+        LIB = lib or os.path.join(HERE, "libsparge_" + "_".join(d.lower() for d in defines) + ".so")
     os.makedirs(BUILD, exist_ok=True)
+    extra = [f"-D{d}" for d in defines]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "sparge.h"))
     objs = []
@@ -43,7 +51,7 @@ def build(verbose=False, force=False):
         objs.append(obj)
         if not force and not _needs(obj, [path] + headers):
             continue
-        cmd = [NVCC] + ARCH + COMMON + ["-c", path, "-o", obj]
+        cmd = [NVCC] + ARCH + COMMON + extra + ["-c", path, "-o", obj]
         if src.endswith(".cpp"):
             cmd += ["-x", "c++"]
         if verbose and src.endswith(".cu"):
@@ -61,5 +69,5 @@ def build(verbose=False, force=False):
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force="--force" in sys.argv)
-    print(LIB)
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv, defines=defs))

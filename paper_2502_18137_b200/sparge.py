@@ -13,7 +13,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparge.so")
+# SPARGE_LIB selects an instrumented build of the same sources (debug only)
+LIB_PATH = os.path.join(_HERE, os.environ.get("SPARGE_LIB", "libsparge.so"))
 
 SPARGE_OK, SPARGE_EINVAL, SPARGE_EINTERNAL, SPARGE_ECUDA, SPARGE_ENOTIMPL = 0, 2, 3, 4, 5
 SPARGE_BF16, SPARGE_FP16 = 0, 1

@@ -20,19 +20,26 @@
 //             QK(t) is issued right after P~V(t-2) (in-order tensor pipe).
 //             The P~V MMA is skipped when all four row groups vote to skip
 //             (their P~ rows are zero otherwise: exact).
-//   warps 0-3 softmax: thread r owns row r == TMEM lane r; warp w is the
-//             gate group I_w (rows 32w..32w+31).  exp2 domain (lambda
-//             compared as lambda*log2e); the gate max is a warp vote
-//             (max_r gap_r > lambda <=> any_r gap_r > lambda); integer row
-//             max; exact int->fp32 via the 1.5*2^23 magic constant folded
-//             into the FFMA bias (R23); packed f32x2 arithmetic; 1 pair in
-//             8 of the exponentials on the FMA pipe (exp2_poly2); P~ (bf16)
-//             written back into the first 32 columns of its own S buffer;
-//             lazy O rescale (R22: the reference max moves only when the
-//             true max grows by > 8 in log2 units; O/l is invariant to the
-//             reference, the gate always uses the true running max).
-//   (profiles/experiments/k_attn_v3_splitrow_speculative.cu: a variant with
-//   rows split over 8 softmax warps -- correct, but slower at 96 registers.)
+//   warps 0-7 softmax.  One warp per SMSP reaches only half the MUFU (ex2)
+//             rate (scripts/ubench_mufu_warps.cu), so every row is split
+//             across two warps: warp w owns TMEM lane quadrant q = w % 4
+//             (rows 32q..32q+31 = the gate group I_q) and column half
+//             h = w / 4 of each 64-key tile -> 4 softmax warps per SMSP with
+//             2 CTAs.  Per tile a warp: loads its 32 S columns, takes the
+//             integer half-row max, publishes it, computes its 32 exp2
+//             values SPECULATIVELY against the current reference max m_ref,
+//             then reads the partner's half max (one 64-thread named
+//             barrier), forms m_local/m_new, votes the lambda gate
+//             (max_r gap_r > lambda <=> any_r gap_r > lambda) and, only if
+//             the reference must move (lazy rescale R22: the true max grew
+//             by > 8 in log2 units, or the row had no reference yet),
+//             recomputes the exponentials.  P~ (bf16) is written into the
+//             half's own S columns [32h, 32h+16) -- never columns the
+//             partner still reads -- and the P~V MMA addresses both pieces.
+//             Exact int->fp32 via the 1.5*2^23 magic constant, folded into
+//             the FFMA bias (R23); packed f32x2 arithmetic; per-half partial
+//             row sums combined in the epilogue; O rescale and epilogue split
+//             O's columns by half.
 #include <cuda.h>
 #include <cstdint>
 #include <climits>
@@ -54,7 +61,7 @@ constexpr int BQ = 128;
 constexpr int BK = 64;
 constexpr int KST = 4;        // K^ stages
 constexpr int VST = 3;        // V^T stages
-constexpr int NSOFT = 4;      // softmax warps: one per TMEM lane quadrant
+constexpr int NSOFT = 8;      // softmax warps: 2 per TMEM lane quadrant
 constexpr int WARP_LOAD = NSOFT, WARP_MMA = NSOFT + 1;
 constexpr int NTHREADS = (NSOFT + 2) * 32;
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
@@ -63,7 +70,7 @@ constexpr int kMagic = 0x4B400000;          // bits of 1.5 * 2^23
 constexpr float kMagicF = 12582912.0f;
 
 #ifndef SPARGE_POLY_EVERY
-#define SPARGE_POLY_EVERY 8
+#define SPARGE_POLY_EVERY 0
 #endif
 constexpr int kPolyEvery = SPARGE_POLY_EVERY;   // one pair in kPolyEvery uses exp2_poly2 (0: none)
 
@@ -151,7 +158,7 @@ __device__ __forceinline__ uint32_t pack16(float lo, float hi) {
   return F16 ? pack_f16x2(lo, hi) : pack_bf16x2(lo, hi);
 }
 
-// P~ = exp2(acc * c - m_ref) for the 64 columns of a row, packed to 16-bit,
+// P~ = exp2(acc * c - m_ref) for this warp's 32 columns, packed to 16-bit,
 // and their sum.  bits(acc + 0x4B400000) are the fp32 value M + acc,
 // M = 1.5*2^23, exactly for |acc| < 2^22 (|acc| <= 127^2 d); one FFMA gives
 //   (M + acc) c - (M c + m_ref) = acc c - m_ref + e,
@@ -160,7 +167,7 @@ __device__ __forceinline__ uint32_t pack16(float lo, float hi) {
 // integer accumulator, far below the INT8 quantisation error in acc (R23).
 // MASKED: INT_MIN entries and rows without a finite reference give 0.
 template <bool MASKED, bool F16>
-__device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, uint32_t* pw,
+__device__ __forceinline__ void exps32(const int32_t* a, float c, float m_ref, uint32_t* pw,
                                        float& sum) {
   const uint64_t c2 = pk(c, c);
   const float nbias = fmaf(-kMagicF, c, -m_ref);
@@ -168,7 +175,7 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
   const bool row_live = m_ref > -INFINITY;
   uint64_t rs2[2] = {0ull, 0ull};
 #pragma unroll
-  for (int k = 0; k < BK; k += 2) {
+  for (int k = 0; k < 32; k += 2) {
     const uint64_t x2 = fma2(pk(__int_as_float(a[k] + kMagic), __int_as_float(a[k + 1] + kMagic)),
                              c2, nb2);
     uint64_t e2;
@@ -279,10 +286,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
                           pv_flag[pb * 4 + 2] | pv_flag[pb * 4 + 3]) != 0;
         if (any) {
           const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
-          const uint32_t tP = tS0 + pb * BK;     // P~ bf16, 32 packed columns
+          // P~ keys 0..31 sit in S columns [0, 16), keys 32..63 in [32, 48)
+          const uint32_t tP = tS0 + pb * BK;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
-            mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
+            mma_f16_ts(tO, tP + (kk >> 1) * 32 + (kk & 1) * 8, dV + 2 * kk, IDESC_PV, 1u);
           ++issued;
         }
         tc_commit(v_empty + vs);
@@ -309,17 +317,22 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     }
   } else {
     // ============================ softmax warps ===========================
-    const int r = threadIdx.x;                 // row within the tile == TMEM lane
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const int q = warp & 3, h = warp >> 2;
+    const int r = q * 32 + lane;               // row within the tile == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     const int row_g = i * BQ + r;
     const bool row_valid = row_g < p.N;
     const bool tile_tail = (i * BQ + BQ > p.N);
+    int* xch = reinterpret_cast<int*>(smem + L::OFF_XCH);      // [2][2][BQ]
+    float* lx = reinterpret_cast<float*>(smem + L::OFF_L);     // [2][BQ]
+    constexpr int DH = D / 2;                   // O columns owned by this half
+    const uint32_t tOh = tO + h * DH + lane_base;
     {
       uint32_t z[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) z[k] = 0u;
 #pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) tmem_st32(tO + lane_base + cc * 32, z);
+      for (int cc = 0; cc < DH / 32; ++cc) tmem_st32(tOh + cc * 32, z);
       tmem_wait_st();
     }
     const float* dk_row = p.dk + static_cast<int64_t>(bkv) * p.T_n;
@@ -351,97 +364,100 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       const int j = __shfl_sync(0xffffffffu, cj, tl);
       const float c = __shfl_sync(0xffffffffu, cc_, tl);
       const int sb = t & 1;
-      const uint32_t tS = tS0 + sb * BK + lane_base;
+      const uint32_t tS = tS0 + sb * BK + lane_base + 32 * h;
 
       PT_MARK(0);
       mbar_wait(s_full + sb, (t >> 1) & 1);
       PT_MARK(1);
       tc_fence_after();
-      int32_t a[BK];
+      int32_t a[32];
       tmem_ld32(tS, reinterpret_cast<uint32_t*>(a));
-      tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(a) + 32);
       tmem_wait_ld();
       PT_MARK(6);
 
       // ---- masking of boundary tiles: keys >= N, causal keys > query, rows >= N
-      const int k0 = j * BK;
-      const bool need_mask = tile_tail || (k0 + BK > p.N) || (CAUSAL && (k0 + BK - 1 > i * BQ));
+      const int k0 = j * BK + 32 * h;
+      const bool need_mask = tile_tail || (j * BK + BK > p.N) || (CAUSAL && (j * BK + BK - 1 > i * BQ));
       if (need_mask) {
         const int kmax = CAUSAL ? min(p.N - 1, row_g) : p.N - 1;
 #pragma unroll
-        for (int k = 0; k < BK; ++k)
+        for (int k = 0; k < 32; ++k)
           if (!row_valid || k0 + k > kmax) a[k] = INT_MIN;
       }
-      // integer-domain row max (monotone: the dequant scale c > 0), eight
-      // independent chains
-      int m8[8];
+      // integer-domain half-row max (monotone: the dequant scale c > 0)
+      int m4[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) m8[u] = max(a[u], a[u + 8]);
+      for (int u = 0; u < 4; ++u) m4[u] = max(a[u], a[u + 4]);
 #pragma unroll
-      for (int k = 16; k < BK; k += 16)
+      for (int k = 8; k < 32; k += 8)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) m8[u] = max(m8[u], max(a[k + u], a[k + 8 + u]));
-      const int mx = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])),
-                         max(max(m8[4], m8[5]), max(m8[6], m8[7])));
-      // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32 through
-      // the magic constant (I2F runs on the slow XU pipe)
+        for (int u = 0; u < 4; ++u) m4[u] = max(m4[u], max(a[k + u], a[k + 4 + u]));
+      const int mh = max(max(m4[0], m4[1]), max(m4[2], m4[3]));
+      xch[(sb * 2 + h) * BQ + r] = mh;
+      PT_MARK(2);
+
+      // ---- speculative P~ against the current reference max ----
+      uint32_t pw[16];
+      float rsum;
+      if (need_mask) exps32<true, F16>(a, c, m_ref, pw, rsum);
+      else exps32<false, F16>(a, c, m_ref, pw, rsum);
+      PT_MARK(4);
+
+      // ---- full-row max from the partner half, gate, lazy rescale ----
+      named_bar_sync(1 + q, 64);
+      const int mx = max(mh, xch[(sb * 2 + (h ^ 1)) * BQ + r]);
+      // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32
       const float m_loc = (mx == INT_MIN) ? -INFINITY
                                           : (__int_as_float(mx + kMagic) - kMagicF) * c;
       const float m_new = fmaxf(m_true, m_loc);
       // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
       const bool compute = __any_sync(0xffffffffu, (mx != INT_MIN) && (m_loc - m_new > p.lam2));
-      // lazy rescale (R22): move the reference max only when it lags the
-      // true max by more than the threshold (always when it is -inf)
-      const bool need = compute && (m_new > m_ref + kRescaleThreshold);
-      const bool rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
-      float alpha = 1.f;
-      if (need) {
-        alpha = ex2_approx(m_ref - m_new);   // 0 when m_ref = -inf (l, O are 0 then)
-        l *= alpha;
-        m_ref = m_new;
-      }
-      m_true = m_new;
-      PT_MARK(2);
-
-      // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ into TMEM ----
-      uint32_t pw[BK / 2];
-      float rsum;
-      if (need_mask) exps64<true, F16>(a, c, m_ref, pw, rsum);
-      else exps64<false, F16>(a, c, m_ref, pw, rsum);
-      l += rsum;           // R9: skipped groups still add their mass to l
-      if (!compute) {
+      const bool need = compute && (m_new > m_ref + kRescaleThreshold);   // also when m_ref = -inf
+      if (__any_sync(0xffffffffu, need)) {
+        // the reference moves for some rows of this group: rescale their l,
+        // redo the exponentials against the new reference, and rescale this
+        // half's O columns once the last issued P~V has landed
+        const bool had_ref = m_ref > -INFINITY;
+        const float alpha = need ? ex2_approx(m_ref - m_new) : 1.f;   // 0 if no ref yet
+        if (need) {
+          l *= alpha;
+          m_ref = m_new;
+        }
+        if (need_mask) exps32<true, F16>(a, c, m_ref, pw, rsum);
+        else exps32<false, F16>(a, c, m_ref, pw, rsum);
+        if (__any_sync(0xffffffffu, need && had_ref)) {
+          if (t >= 1) mbar_wait(o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < BK / 2; ++k) pw[k] = 0u;
-      }
-      PT_MARK(4);
-
-      if (rescale_o) {
-        // O rows of this warp hold P~V of earlier tiles: wait for the last
-        // issued P~V, then rescale in TMEM (before p_full(t) releases P~V(t)).
-        if (t >= 1) mbar_wait(o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
-        tc_fence_after();
+          for (int cc = 0; cc < DH / 32; ++cc) {
+            uint32_t ov[32];
+            tmem_ld32(tOh + cc * 32, ov);
+            tmem_wait_ld();
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
-          uint32_t ov[32];
-          tmem_ld32(tO + lane_base + cc * 32, ov);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
-          tmem_st32(tO + lane_base + cc * 32, ov);
+            for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
+            tmem_st32(tOh + cc * 32, ov);
+          }
         }
       }
+      m_true = m_new;
+      l += rsum;           // R9: skipped groups still add their mass to l
       PT_MARK(3);
 
-      // P~(t) overwrites the first 32 columns of S[sb]: S(t) is already in
-      // registers, and QK(t) -- complete, per s_full -- executed after
-      // P~V(t-2), the previous reader of this buffer.
-      tmem_st32(tS, pw);
+      if (!compute) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) pw[k] = 0u;
+      }
+      // P~(t) goes into this half's own S columns [32h, 32h+16): only this
+      // warp read them (S(t) is in registers); QK(t) -- complete, per
+      // s_full -- executed after P~V(t-2), the previous reader.
+      tmem_st16(tS, pw);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + warp)),
-                     "r"(compute ? 1u : 0u) : "memory");
+        if (h == 0)
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + q)),
+                       "r"(compute ? 1u : 0u) : "memory");
         mbar_arrive(p_full + sb);
       }
       if (compute) ++slices;
@@ -454,16 +470,19 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 #endif
 
     // ---- epilogue: O_i = O / l (line 19), scattered back through perm ----
+    lx[h * BQ + r] = l;
+    named_bar_sync(1 + q, 64);
+    l += lx[(h ^ 1) * BQ + r];
     if (n_tiles > 0) mbar_wait(o_done + ((n_tiles - 1) & 1), ((n_tiles - 1) >> 1) & 1);
     tc_fence_after();
-    if (row_valid && !(l > 0.f)) atomicOr(p.status, 1u);
+    if (h == 0 && row_valid && !(l > 0.f)) atomicOr(p.status, 1u);
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
     const int dst_row = row_valid ? (p.perm ? __ldg(p.perm + row_g) : row_g) : 0;
-    uint16_t* orow = p.o + b * p.o_sb + hq * p.o_sh + static_cast<int64_t>(dst_row) * p.o_sn;
+    uint16_t* orow = p.o + b * p.o_sb + hq * p.o_sh + static_cast<int64_t>(dst_row) * p.o_sn + h * DH;
 #pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
+    for (int cc = 0; cc < DH / 32; ++cc) {
       uint32_t ov[32];
-      tmem_ld32(tO + lane_base + cc * 32, ov);
+      tmem_ld32(tOh + cc * 32, ov);
       tmem_wait_ld();
       if (row_valid) {
 #pragma unroll
@@ -479,7 +498,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       }
     }
     if (p.counters) {
-      if (lane == 0) atomicAdd(p.counters + bhq * 3 + 1, static_cast<unsigned long long>(slices));
+      if (lane == 0 && h == 0) atomicAdd(p.counters + bhq * 3 + 1, static_cast<unsigned long long>(slices));
       if (threadIdx.x == 0) atomicAdd(p.counters + bhq * 3 + 0, static_cast<unsigned long long>(n_tiles));
     }
   }
