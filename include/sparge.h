@@ -123,7 +123,8 @@ int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_s
  *   lut   int32 [B, Hq, T_m, T_n]: kept j of row i in ascending order
  *   cnt   int32 [B, Hq, T_m]: number of kept j of row i (>= 1)
  * tau in (0, 1], theta in [-1, 1] (float32, compared in fp64).
- * Errors: SPARGE_EINVAL (range / NULL / T_n > 4096), SPARGE_ECUDA.
+ * Errors: SPARGE_EINVAL (range / NULL / T_n > 2048, i.e. N > 131072),
+ * SPARGE_ECUDA.
  */
 int sparge_predict_mask(const sparge_shape* shape,
                         const double* q_pooled, const double* q_sim,

@@ -118,7 +118,7 @@ int sparge_predict_mask(const sparge_shape* shape, const double* q_pooled, const
   if (!(tau > 0.f && tau <= 1.f)) return SPARGE_EINVAL;
   if (!(theta >= -1.f && theta <= 1.f)) return SPARGE_EINVAL;
   const int T_n = (shape->N + shape->bk - 1) / shape->bk;
-  if (T_n > 4096) return SPARGE_EINVAL;
+  if (T_n > 2048) return SPARGE_EINVAL;   // one shared-memory row of 2048 (N <= 131072)
   cudaError_t e = launch_predict(*shape, q_pooled, q_sim, k_pooled, k_sim, tau, theta, mask, lut,
                                  cnt, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
