@@ -61,6 +61,18 @@ constexpr float kRescaleThreshold = 8.0f;   // log2 units
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kMagic = 0x4B400000;          // bits of 1.5 * 2^23
 constexpr float kMagicF = 12582912.0f;
+// S pre-bias: the MMA warp fills S with 0x4B400000 (tcgen05.cp from a
+// constant shared-memory tile) before the accumulating INT8 QK MMAs, so the
+// int32 accumulator holds bits(1.5*2^23 + acc) -- the exact fp32 value --
+// and the softmax needs no per-element integer add (kAddMagic = 0).
+// Measured slower (Llama 32K attention 3.93 -> 5.19 ms): the 32 KB
+// smem->TMEM copy per tile occupies the in-order tensor pipe for ~256
+// cycles.  Off by default; kept as a recorded experiment.
+#ifndef SPARGE_S_BIAS
+#define SPARGE_S_BIAS 0
+#endif
+constexpr int kAddMagic = SPARGE_S_BIAS ? 0 : kMagic;
+constexpr int kCBiasBytes = 8192;           // constant tile read by tcgen05.cp
 
 #ifndef SPARGE_POLY_EVERY
 #define SPARGE_POLY_EVERY 8
@@ -80,7 +92,8 @@ struct Smem {
   static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;
   static constexpr int OFF_XCH = OFF_MISC + 64;             // int [2 bufs][2 halves][BQ]
   static constexpr int OFF_L = OFF_XCH + 2 * 2 * BQ * 4;   // float [2 halves][BQ]
-  static constexpr int TOTAL = OFF_L + 2 * BQ * 4;
+  static constexpr int OFF_CB = ((OFF_L + 2 * BQ * 4) + 127) / 128 * 128;   // u32[kCBiasBytes/4]
+  static constexpr int TOTAL = OFF_CB + kCBiasBytes;
   static constexpr int ALLOC = TOTAL + 1024;     // slack for 1024-B alignment
   static constexpr int ROW_BYTES_QK = D;          // 128 -> SW128, 64 -> SW64
 };
@@ -167,9 +180,34 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
   const uint64_t nb2 = pk(nbias, nbias);
   const bool row_live = m_ref > -INFINITY;
   uint64_t rs2[2] = {0ull, 0ull};
+#ifdef SPARGE_EXP_PHASED
+  if (!MASKED) {
+    // three explicit phases: all exponent arguments, a burst of independent
+    // MUFU ex2 (plus the FMA-pipe pairs), then sums and packs
+    uint64_t x2[BK / 2];
+#pragma unroll
+    for (int k = 0; k < BK; k += 2)
+      x2[k >> 1] = fma2(pk(__int_as_float(a[k] + kAddMagic), __int_as_float(a[k + 1] + kAddMagic)), c2, nb2);
+#pragma unroll
+    for (int u = 0; u < BK / 2; ++u) {
+      if (kPolyEvery > 0 && (u % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
+        x2[u] = exp2_poly2(x2[u]);
+      else
+        x2[u] = pk(ex2_approx(lo_f(x2[u])), ex2_approx(hi_f(x2[u])));
+    }
+#pragma unroll
+    for (int u = 0; u < BK / 2; ++u) {
+      rs2[u & 1] = add2(rs2[u & 1], x2[u]);
+      pw[u] = pack16<F16>(lo_f(x2[u]), hi_f(x2[u]));
+    }
+    const uint64_t rs = add2(rs2[0], rs2[1]);
+    sum = lo_f(rs) + hi_f(rs);
+    return;
+  }
+#endif
 #pragma unroll
   for (int k = 0; k < BK; k += 2) {
-    const uint64_t x2 = fma2(pk(__int_as_float(a[k] + kMagic), __int_as_float(a[k + 1] + kMagic)),
+    const uint64_t x2 = fma2(pk(__int_as_float(a[k] + kAddMagic), __int_as_float(a[k + 1] + kAddMagic)),
                              c2, nb2);
     uint64_t e2;
     if (!MASKED && kPolyEvery > 0 && ((k >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
@@ -232,6 +270,12 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     }
     fence_mbar_init();
   }
+  if (SPARGE_S_BIAS) {
+    uint4* cb = reinterpret_cast<uint4*>(smem + L::OFF_CB);
+    for (int e = threadIdx.x; e < kCBiasBytes / 16; e += NTHREADS)
+      cb[e] = make_uint4(kMagic, kMagic, kMagic, kMagic);
+    fence_proxy_async_smem();     // generic writes -> tcgen05.cp (async proxy)
+  }
   if (warp == WARP_MMA) tmem_alloc<256>(tmem_base_slot);
   tc_fence_before();
   __syncthreads();
@@ -267,6 +311,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       constexpr uint32_t IDESC_QK = idesc_i8(BQ, BK);
       constexpr uint32_t IDESC_PV = F16 ? idesc_f16(BQ, D) : idesc_bf16(BQ, D);
       const uint64_t dQ = umma_desc_kmajor(smem_u32(sQ), L::ROW_BYTES_QK);
+      // no-swizzle descriptor over the constant tile (LBO 128 B, SBO 256 B;
+      // every byte it can address holds the bias pattern)
+      const uint64_t cb_desc = static_cast<uint64_t>((smem_u32(smem + L::OFF_CB) >> 4) & 0x3FFFu) |
+                               (static_cast<uint64_t>(128 >> 4) << 16) |
+                               (static_cast<uint64_t>(256 >> 4) << 32) | (1ull << 46);
       unsigned long long issued = 0;
       mbar_wait(q_full, 0);
       tc_fence_after();
@@ -297,9 +346,18 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         // reading S(t-2) before they arrived on p_full(t-2)).
         tc_fence_after();
         const uint64_t dK = umma_desc_kmajor(smem_u32(sK + ks * L::K_BYTES), L::ROW_BYTES_QK);
+        if (SPARGE_S_BIAS) {
+          // S[sb] = 0x4B400000 everywhere (8 x 128 lanes x 8 columns), in
+          // tensor-pipe order after P~V(t-2) and before QK(t)
+#pragma unroll
+          for (int cc = 0; cc < BK / 8; ++cc)
+            asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;"
+                         ::"r"(tS0 + sb * BK + 8 * cc), "l"(cb_desc) : "memory");
+        }
 #pragma unroll
         for (int kk = 0; kk < D / 32; ++kk)       // K = 32 per kind::i8 MMA (32 B)
-          mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, kk > 0 ? 1u : 0u);
+          mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK,
+                 (SPARGE_S_BIAS || kk > 0) ? 1u : 0u);
         tc_commit(s_full + sb);
         tc_commit(k_empty + ks);
         if (t > 0) do_pv(t - 1);
@@ -386,7 +444,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32 through
       // the magic constant (I2F runs on the slow XU pipe)
       const float m_loc = (mx == INT_MIN) ? -INFINITY
-                                          : (__int_as_float(mx + kMagic) - kMagicF) * c;
+                                          : (__int_as_float(mx + kAddMagic) - kMagicF) * c;
       const float m_new = fmaxf(m_true, m_loc);
       // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
       const bool compute = __any_sync(0xffffffffu, (mx != INT_MIN) && (m_loc - m_new > p.lam2));
