@@ -326,15 +326,14 @@ def run_ours(args):
         Ke = min(K, 10)
         eve = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(Ke)]
-        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        # the public host-buffer entry point: kv-head chunks with H2D copy,
+        # compute and D2H copy on separate streams (sparge.HostPipeline)
+        pipe = sparge.HostPipeline(1, Hq, Hkv, N, d, causal=cfg["causal"], dtype=q.dtype,
+                                   chunks=max(c for c in (1, 2, 3, 4, 6, 8) if Hkv % c == 0),
+                                   device=dev)
 
         def e2e_step():
-            qd.copy_(qh, non_blocking=True)
-            kd.copy_(kh, non_blocking=True)
-            vd.copy_(vh, non_blocking=True)
-            sparge.sparge_forward(qd, kd, vd, tau, theta, lam, causal=cfg["causal"], perm=perm,
-                                  buffers=bf, out=o)
-            oh.copy_(o, non_blocking=True)
+            pipe(qh, kh, vh, oh, tau, theta, lam, perm=perm)
 
         e2e_step()
         torch.cuda.synchronize()

@@ -194,3 +194,66 @@ def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=No
     sparge_attn_fwd(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm, o,
                     bf.counters, bf.workspace, stream)
     return o, bf
+
+
+class HostPipeline:
+    """End-to-end SpargeAttn from pinned HOST buffers with copy/compute overlap.
+
+    The (batch, kv-head group) problems are independent, so
+    the work is split into `chunks` groups of kv-heads: chunk c's host->device
+    copy runs on one stream, its five kernels (quantise Q, K; predict; V
+    stage; attention) on a second, and its O device->host copy on a third,
+    overlapping with the neighbouring chunks.  Device buffers are allocated
+    once.  All compute is the C-ABI kernels; this class only orchestrates
+    copies and streams (torch)."""
+
+    def __init__(self, B, Hq, Hkv, N, d, causal=False, dtype=torch.bfloat16, chunks=4,
+                 device="cuda", sim_mode=SPARGE_SIM_COSINE):
+        if Hkv % chunks:
+            chunks = 1
+        self.B, self.Hq, self.Hkv, self.N, self.d = B, Hq, Hkv, N, d
+        self.group = Hq // Hkv
+        self.chunks = chunks
+        self.kv_per = Hkv // chunks
+        self.q_per = self.kv_per * self.group
+        self.shape = make_shape(B, self.q_per, self.kv_per, N, d, causal, dtype, sim_mode)
+        kw = dict(device=device, dtype=dtype)
+        self.q = torch.empty(B, Hq, N, d, **kw)
+        self.k = torch.empty(B, Hkv, N, d, **kw)
+        self.v = torch.empty(B, Hkv, N, d, **kw)
+        self.o = torch.empty(B, Hq, N, d, **kw)
+        self.bufs = [Buffers(self.shape, device=device, with_mask=False) for _ in range(min(chunks, 2))]
+        self.s_h2d = torch.cuda.Stream(device)
+        self.s_comp = torch.cuda.Stream(device)
+        self.s_d2h = torch.cuda.Stream(device)
+
+    def __call__(self, qh, kh, vh, oh, tau, theta, lam, perm=None):
+        """qh/kh/vh: pinned host [B,H,N,d]; oh: pinned host output.  Enqueues
+        everything after the current stream's pending work and makes the
+        current stream wait for the final copy."""
+        cur = torch.cuda.current_stream()
+        for s in (self.s_h2d, self.s_comp, self.s_d2h):
+            s.wait_stream(cur)
+        done_prev_comp = None
+        for c in range(self.chunks):
+            qs = slice(c * self.q_per, (c + 1) * self.q_per)
+            ks = slice(c * self.kv_per, (c + 1) * self.kv_per)
+            with torch.cuda.stream(self.s_h2d):
+                self.q[:, qs].copy_(qh[:, qs], non_blocking=True)
+                self.k[:, ks].copy_(kh[:, ks], non_blocking=True)
+                self.v[:, ks].copy_(vh[:, ks], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(self.s_h2d)
+            bf = self.bufs[c % len(self.bufs)]
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(ev_in)
+                sparge_forward(self.q[:, qs], self.k[:, ks], self.v[:, ks], tau, theta, lam,
+                               causal=bool(self.shape.causal), perm=perm, buffers=bf,
+                               out=self.o[:, qs], stream=self.s_comp)
+                ev_out = torch.cuda.Event()
+                ev_out.record(self.s_comp)
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(ev_out)
+                oh[:, qs].copy_(self.o[:, qs], non_blocking=True)
+        cur.wait_stream(self.s_d2h)
+        return oh

@@ -178,3 +178,17 @@ def test_lambda_gate_fires_and_matches(lib):
     assert abs(int(c[1]) - ref["cnt"]["pv_slices"]) <= 4
     assert int(c[2]) <= int(c[0])
     assert rel_l1(bf16_np(o)[0, 0], ref["o"]) < BUG_L1
+
+
+def test_host_pipeline_matches_device_path(lib):
+    """The pipelined host-buffer entry point (kv-head chunks on separate copy
+    and compute streams) gives exactly the one-shot device path's O."""
+    N, d, Hq, Hkv = 1500, 128, 8, 4
+    qn, kn, vn = inputs.llm_local(77, N, d=d, Hq=Hq, Hkv=Hkv)
+    qh, kh, vh = (inputs.to_device(a, device="cpu", pin=True) for a in (qn, kn, vn))
+    o_ref, _ = lib.sparge_forward(qh.cuda(), kh.cuda(), vh.cuda(), 0.9, 0.5, -5.0, causal=True)
+    pipe = lib.HostPipeline(1, Hq, Hkv, N, d, causal=True, chunks=2)
+    oh = torch.empty_like(qh).pin_memory()
+    pipe(qh, kh, vh, oh, 0.9, 0.5, -5.0)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, o_ref.cpu())
