@@ -201,7 +201,7 @@ def run_ours(args):
         sparge.sparge_quantize(shape, k_, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim)
         if ev: ev[1].record()
         sparge.sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, t, th,
-                                   bf.mask, bf.lut, bf.cnt)
+                                   bf.mask, bf.lut, bf.cnt, bf.pred_workspace)
         if ev: ev[2].record()
         sparge.sparge_attn_fwd_ex(shape, bf.qq, bf.dq, bf.kq, bf.dk, v_, bf.lut, bf.cnt, lm, perm,
                                   o_, counters, bf.workspace, sparge.SPARGE_ATTN_VPREP_ONLY)

@@ -122,6 +122,8 @@ int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_s
  *   mask  nullable uint8 [B, Hq, T_m, T_n]  (M_g of Definition 1)
  *   lut   int32 [B, Hq, T_m, T_n]: kept j of row i in ascending order
  *   cnt   int32 [B, Hq, T_m]: number of kept j of row i (>= 1)
+ *   workspace/ws_bytes  >= sparge_predict_workspace(shape), 256-byte aligned
+ *         (scratch for S^; contents undefined on return)
  * tau in (0, 1], theta in [-1, 1] (float32, compared in fp64).
  * Errors: SPARGE_EINVAL (range / NULL / T_n > 2048, i.e. N > 131072),
  * SPARGE_ECUDA.
@@ -131,7 +133,11 @@ int sparge_predict_mask(const sparge_shape* shape,
                         const double* k_pooled, const double* k_sim,
                         float tau, float theta,
                         uint8_t* mask, int32_t* lut, int32_t* cnt,
-                        void* stream);
+                        void* workspace, size_t ws_bytes, void* stream);
+
+/* Bytes of device workspace sparge_predict_mask needs (the fp64 compressed
+ * map S^, B*Hq*T_m*T_n doubles).  0 on invalid shape. */
+size_t sparge_predict_workspace(const sparge_shape* shape);
 
 /* Bytes of device workspace sparge_attn_fwd needs for `shape` (V^T staging,
  * work list, status word).  0 on invalid shape. */

@@ -1,27 +1,25 @@
-// k_predict_topcdf -- step a2 of the hot path.
+// Stage 1 of Algorithm 1 -- step a2 of the hot path.
 //
-// One CTA per (8 query blocks, q-head, batch).  From the a1 statistics it
-// forms the rows of the compressed attention map and the block mask M_g:
-//   S^[j] = q_i . k_j / sqrt(d)                 Alg. 1 line 5, R2
-//   S^[j] = -inf if s_kj < theta (strict, R5) or tile (i,j) causally dead (R8)
-//   P^   = softmax(S^)                          line 6
-//   M[i,:] = TopCdf(P^, tau)                    §3.2 pseudocode, R4:
+//   S^[i,j] = q_i . k_j / sqrt(d)                 Alg. 1 line 5, R2
+//   S^[i,j] = -inf if s_kj < theta (strict, R5) or tile (i,j) causally dead (R8)
+//   P^[i]  = softmax(S^[i])                       line 6
+//   M[i,:] = TopCdf(P^[i], tau)                   §3.2 pseudocode, R4:
 //       order (P^ desc, j asc); keep rank k iff cumsum_k <= tau*c_last;
 //       always keep rank 0 (guard)
 //   M[i,:] = 1 if s_qi < theta; M[:,j] = 1 if s_kj < theta    Eq. 5
 //   all -inf row -> all ones (R7); causal: M &= live, M[i, i*bq/bk] = 1 (R8)
-// and compacts the kept j (ascending) into the LUT the attention kernel
-// walks.  Everything is fp64 (R15).
+// plus the compaction of the kept j (ascending) into the LUT the attention
+// kernel walks.  Everything is fp64 (R15).
 //
-// Phase A (all 8 warps): S^ for the CTA's 8 rows.  The pooled keys of the
-//   kv-head stream through shared memory in 32-row chunks (cp.async, double
-//   buffered, rows padded to d+1 doubles: conflict-free), so each chunk is
-//   read from L2 once per 8 query blocks; warp w computes row w, lane l key
-//   j0+l.
-// Phase B (warp w owns row w): softmax, warp-synchronous bitonic sort of
-//   (P^ desc, j asc) in shared memory, warp scan, threshold, forcing,
-//   causal AND + guard, ballot compaction into the LUT.
-// Bound: fp64 FMA + shared memory; no block-wide barrier in phase B.
+// k_shat_dmma   S^ = Q^-bar K^-bar^T / sqrt(d) per head on the fp64 tensor
+//               cores (mma.sync m8n8k4 f64, DMMA): 64 query blocks x 64 key
+//               blocks per CTA staged in shared memory (rows padded to d+4
+//               doubles: the A/B fragment loads are bank-conflict free), one
+//               8-row strip per warp; written to the workspace.
+// k_topcdf_rows one warp per (head, query block): masks, softmax, a
+//               warp-synchronous branch-free bitonic sort of 64-bit composite
+//               keys in shared memory, a conflict-free warp scan, threshold,
+//               forcing, causal AND + guard, ballot compaction into the LUT.
 #include <cstdint>
 #include <cfloat>
 
@@ -31,12 +29,106 @@ namespace sparge {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kRows = 8;         // query blocks per CTA (one per warp in phase B)
-constexpr int kChunk = 32;       // pooled keys per shared-memory chunk
+// ---------------------------------------------------------------- S^ GEMM
+constexpr int kTile = 64;          // query blocks x key blocks per CTA
+constexpr int kGemmThreads = 256;  // 8 warps, one 8-row strip each
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+               ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kGemmThreads)
+k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_pooled,
+            int Hq, int Hkv, int T_m, int T_n, double* __restrict__ shat) {
+  constexpr int KR = D + 4;         // padded row (doubles): KR % 16 == 4
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sq = reinterpret_cast<double*>(smem);          // [kTile][KR]
+  double* sk = sq + kTile * KR;                          // [kTile][KR]
+  const int j0 = blockIdx.x * kTile, i0 = blockIdx.y * kTile, bhq = blockIdx.z;
+  const int hq = bhq % Hq, b = bhq / Hq;
+  const int hkv = hq / (Hq / Hkv);
+  const int64_t qbase = static_cast<int64_t>(bhq) * T_m;
+  const int64_t kbase = (static_cast<int64_t>(b) * Hkv + hkv) * T_n;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+  // stage 64 pooled-Q rows and 64 pooled-K rows (zero beyond T_m / T_n)
+  constexpr int CH = D / 2;         // 16-B chunks per row
+  for (int e = tid; e < 2 * kTile * CH; e += kGemmThreads) {
+    const int which = e / (kTile * CH);
+    const int rr = (e / CH) % kTile, cc = e % CH;
+    double* dst = (which ? sk : sq) + rr * KR + 2 * cc;
+    const bool ok = which ? (j0 + rr < T_n) : (i0 + rr < T_m);
+    if (ok) {
+      const double* src = which ? k_pooled + (kbase + j0 + rr) * D + 2 * cc
+                                : q_pooled + (qbase + i0 + rr) * D + 2 * cc;
+      cp_async16(dst, src);
+    } else {
+      dst[0] = 0.0;
+      dst[1] = 0.0;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+
+  // warp wid: rows 8*wid..8*wid+7 against all 64 keys (8 DMMA tiles)
+  // fragments (m8n8k4, f64): A row = lane/4, k = lane%4; B k = lane%4,
+  // n = lane/4; C row = lane/4, cols 2*(lane%4) + {0,1}
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[8][2];
+#pragma unroll
+  for (int kt = 0; kt < 8; ++kt) acc[kt][0] = acc[kt][1] = 0.0;
+  const double* arow = sq + (8 * wid + g) * KR + t4;
+  const double* brow = sk + g * KR + t4;
+#pragma unroll 4
+  for (int ks = 0; ks < D / 4; ++ks) {
+    const double a = arow[4 * ks];
+#pragma unroll
+    for (int kt = 0; kt < 8; ++kt) dmma_884(acc[kt][0], acc[kt][1], a, brow[8 * kt * KR + 4 * ks]);
+  }
+  const double inv_sqrt_d = 1.0 / sqrt(static_cast<double>(D));
+  const int row = i0 + 8 * wid + g;
+  if (row < T_m) {
+    double* out = shat + (qbase + row) * T_n;
+#pragma unroll
+    for (int kt = 0; kt < 8; ++kt) {
+      const int key = j0 + 8 * kt + 2 * t4;
+      if (key < T_n) out[key] = acc[kt][0] * inv_sqrt_d;
+      if (key + 1 < T_n) out[key + 1] = acc[kt][1] * inv_sqrt_d;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- TopCdf rows
+constexpr int kRowWarps = 4;
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
 
 // Warp-synchronous bitonic sort, descending, of SORTN 64-bit keys in shared
-// memory; branch-free compare-exchange, fully unrolled per stage.
+// memory; branch-free compare-exchange, unrolled per stage.
 template <int SORTN>
 __device__ __forceinline__ void sort_desc(uint64_t* key, int lane) {
 #pragma unroll 1
@@ -61,116 +153,34 @@ __device__ __forceinline__ void sort_desc(uint64_t* key, int lane) {
     }
   }
 }
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;"
-               ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-template <int D>
-struct PredSmem {
-  static constexpr int KROW = D + 1;                         // padded pooled-key row (doubles)
-  static constexpr int KBUF = kChunk * KROW;                 // doubles per chunk buffer
-  // layout: q[kRows][D] | kbuf[2][KBUF] (phase A) aliased by idx[kRows][sortn] u16
-  //         (phase B) | key[kRows][sortn] f64 | flag[kRows][sortn] u8
-  static size_t bytes(int sortn) {
-    const size_t q = sizeof(double) * kRows * D;
-    const size_t kb = sizeof(double) * 2 * KBUF;
-    const size_t idx = sizeof(uint16_t) * kRows * sortn;
-    const size_t u = kb > idx ? kb : idx;
-    return q + u + sizeof(double) * kRows * sortn + static_cast<size_t>(kRows) * sortn;
-  }
-};
-
-template <int D>
-__global__ void __launch_bounds__(kThreads)
-k_predict_topcdf(const double* __restrict__ q_pooled, const double* __restrict__ q_sim,
-                 const double* __restrict__ k_pooled, const double* __restrict__ k_sim,
-                 int Hq, int Hkv, int N, int T_m, int T_n, int sortn, int bq, int bk,
-                 int causal, double tau, double theta,
-                 uint8_t* __restrict__ mask, int32_t* __restrict__ lut,
-                 int32_t* __restrict__ cnt) {
-  using L = PredSmem<D>;
+__global__ void __launch_bounds__(kRowWarps * 32)
+k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
+              const double* __restrict__ k_sim, int Hq, int Hkv, int N, int T_m, int T_n,
+              int rows_total, int sortn, int bq, int bk, int causal, double tau, double theta,
+              uint8_t* __restrict__ mask, int32_t* __restrict__ lut, int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* s_q = reinterpret_cast<double*>(smem);                              // [kRows][D]
-  double* s_kb = s_q + kRows * D;                                             // [2][KBUF]
-  const size_t u_bytes = (sizeof(double) * 2 * L::KBUF > sizeof(uint16_t) * kRows * sortn)
-                             ? sizeof(double) * 2 * L::KBUF
-                             : sizeof(uint16_t) * kRows * sortn;
-  double* s_key = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(s_kb) + u_bytes);
-  uint8_t* s_flag = reinterpret_cast<uint8_t*>(s_key + kRows * sortn);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int row = blockIdx.x * kRowWarps + wid;          // (b*Hq + hq)*T_m + i
+  if (row >= rows_total) return;
+  uint64_t* ukey = reinterpret_cast<uint64_t*>(smem) + wid * sortn;
+  double* key = reinterpret_cast<double*>(ukey);
+  uint8_t* flag = smem + static_cast<size_t>(kRowWarps) * sortn * 8 + wid * sortn;
 
-  const int hq = blockIdx.y, b = blockIdx.z;
-  const int hkv = hq / (Hq / Hkv);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int i0 = blockIdx.x * kRows;
-  const int64_t qbase = (static_cast<int64_t>(b) * Hq + hq) * T_m;
-  const int64_t kbase = (static_cast<int64_t>(b) * Hkv + hkv) * T_n;
-  const double sqrt_d = sqrt(static_cast<double>(D));
+  const int i = row % T_m, bhq = row / T_m;
+  const int hq = bhq % Hq, b = bhq / Hq;
+  const int64_t kbase = (static_cast<int64_t>(b) * Hkv + hq / (Hq / Hkv)) * T_n;
+  const int last_q = min((i + 1) * bq, N) - 1;
+  const double* srow = shat + static_cast<int64_t>(row) * T_n;
 
-  // ---------------- phase A: S^ rows ----------------
-  for (int e = tid; e < kRows * D; e += kThreads) {
-    const int rr = e / D;
-    s_q[e] = (i0 + rr < T_m) ? q_pooled[(qbase + i0 + rr) * D + (e % D)] : 0.0;
-  }
-  const int nchunks = (T_n + kChunk - 1) / kChunk;
-  auto issue = [&](int c) {
-    double* dst = s_kb + (c & 1) * L::KBUF;
-    const int j0 = c * kChunk;
-    for (int e = tid; e < kChunk * D; e += kThreads) {
-      const int jj = e / D, dd = e % D;
-      if (j0 + jj < T_n) cp_async8(dst + jj * L::KROW + dd, k_pooled + (kbase + j0 + jj) * D + dd);
-    }
-    cp_async_commit();
-  };
-  issue(0);
-  const int my_row = i0 + wid;
-  const int last_q = min((my_row + 1) * bq, N) - 1;
-  for (int c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) {
-      issue(c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* kc = s_kb + (c & 1) * L::KBUF + lane * L::KROW;
-    const double* qr = s_q + wid * D;
-    double dot0 = 0.0, dot1 = 0.0;
-#pragma unroll 8
-    for (int dd = 0; dd < D; dd += 2) {
-      dot0 = fma(qr[dd], kc[dd], dot0);
-      dot1 = fma(qr[dd + 1], kc[dd + 1], dot1);
-    }
-    const int j = c * kChunk + lane;
-    if (j < T_n && my_row < T_m) {
-      const bool dead = causal && (j * bk > last_q);
-      const bool fix = k_sim[kbase + j] < theta;
-      s_key[wid * sortn + j] = (dead || fix) ? -INFINITY : (dot0 + dot1) / sqrt_d;
-    }
-    __syncthreads();
-  }
-
-  // ---------------- phase B: one warp per row ----------------
-  if (my_row >= T_m) return;
-  double* key = s_key + wid * sortn;
-  uint8_t* flag = s_flag + wid * sortn;
-
+  // ---- S^ row with the -inf columns (fixed K blocks, causally dead) ----
   double mx = -INFINITY;
-  for (int j = lane; j < T_n; j += 32) mx = fmax(mx, key[j]);
+  for (int j = lane; j < T_n; j += 32) {
+    const bool dead = causal && (j * bk > last_q);
+    const double s = (dead || k_sim[kbase + j] < theta) ? -INFINITY : srow[j];
+    key[j] = s;
+    mx = fmax(mx, s);
+  }
   mx = warp_max(mx);
   const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
 
@@ -186,9 +196,8 @@ k_predict_topcdf(const double* __restrict__ q_pooled, const double* __restrict__
     // value order) with the low 11 mantissa bits replaced by 2047 - j.  Sorting
     // the keys descending orders (P^ desc, j asc) up to a 2^-42 relative
     // truncation of P^ -- far inside the 1e-6 near-threshold band of the
-    // parity criterion; the cumulative sum below uses the truncated values.
+    // parity criterion; the cumulative sum uses the truncated values.
     // Padding keys are 0 and sort last (a real entry has key >= 2047 - j > 0).
-    uint64_t* ukey = reinterpret_cast<uint64_t*>(key);
     for (int j = lane; j < sortn; j += 32) {
       ukey[j] = (j < T_n)
                     ? ((static_cast<uint64_t>(__double_as_longlong(key[j] / total)) & ~0x7FFull) |
@@ -205,38 +214,38 @@ k_predict_topcdf(const double* __restrict__ q_pooled, const double* __restrict__
       case 1024: sort_desc<1024>(ukey, lane); break;
       default: sort_desc<2048>(ukey, lane); break;
     }
-    // inclusive cumulative sum in rank order (contiguous chunk per lane):
-    // pass 1 for the chunk totals and c_last, pass 2 for the decisions
-    const int per = sortn / 32;
-    const int k0 = lane * per, k1 = min(T_n, k0 + per);
-    double loc = 0.0;
-    for (int k = k0; k < k1; ++k) loc += __longlong_as_double(ukey[k] & ~0x7FFull);
-    double incl = loc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double tv = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += tv;
+    // inclusive cumulative sum in rank order, 32 ranks per step (rank
+    // 32*s + lane): conflict-free shared-memory reads.  Pass 1 finds c_last,
+    // pass 2 recomputes the identical prefix sums and decides.  c_last (R4)
+    // is the maximum of the computed prefix sums: equal to the last one in
+    // exact arithmetic, and it keeps tau = 1 exact under rounding.
+    const int steps = (T_n + 31) / 32;
+    double carry = 0.0, cmax = 0.0;
+    for (int s = 0; s < steps; ++s) {
+      const int k = 32 * s + lane;
+      const double p = (k < T_n) ? __longlong_as_double(ukey[k] & ~0x7FFull) : 0.0;
+      const double c = carry + warp_incl_scan(p, lane);
+      cmax = fmax(cmax, c);
+      carry = __shfl_sync(0xffffffffu, c, 31);
     }
-    // c_last, the last element of the cumulative sum (R4): the maximum of the
-    // computed prefix sums (equal in exact arithmetic; keeps tau = 1 exact
-    // when the parallel scan's rounding is non-monotone by an ulp)
-    const double cmax = warp_max((k1 > k0) ? incl : 0.0);
-    const double thr = tau * cmax;
-    double cacc = incl - loc;
-    for (int k = k0; k < k1; ++k) {
-      const uint64_t kv = ukey[k];
-      cacc += __longlong_as_double(kv & ~0x7FFull);
-      flag[2047 - static_cast<int>(kv & 0x7FFull)] = (cacc <= thr || k == 0) ? 1 : 0;
+    const double thr = tau * warp_max(cmax);
+    carry = 0.0;
+    for (int s = 0; s < steps; ++s) {
+      const int k = 32 * s + lane;
+      const uint64_t kv = (k < T_n) ? ukey[k] : 0ull;
+      const double p = (k < T_n) ? __longlong_as_double(kv & ~0x7FFull) : 0.0;
+      const double c = carry + warp_incl_scan(p, lane);
+      carry = __shfl_sync(0xffffffffu, c, 31);
+      if (k < T_n) flag[2047 - static_cast<int>(kv & 0x7FFull)] = (c <= thr || k == 0) ? 1 : 0;
     }
     __syncwarp();
   }
 
   // ---- forcing (Eq. 5), flagged rows, causal live AND + diagonal guard ----
-  const int64_t row = qbase + my_row;
   const bool row_fix = q_sim[row] < theta;
-  const int guard = (my_row * bq) / bk;
-  uint8_t* mrow = mask ? mask + row * T_n : nullptr;
-  int32_t* lrow = lut + row * T_n;
+  const int guard = (i * bq) / bk;
+  uint8_t* mrow = mask ? mask + static_cast<int64_t>(row) * T_n : nullptr;
+  int32_t* lrow = lut + static_cast<int64_t>(row) * T_n;
   int base = 0;
   for (int j0 = 0; j0 < T_n; j0 += 32) {
     const int j = j0 + lane;
@@ -257,32 +266,51 @@ k_predict_topcdf(const double* __restrict__ q_pooled, const double* __restrict__
   if (lane == 0) cnt[row] = base;
 }
 
+template <int D>
+cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double* q_sim,
+                     const double* k_pooled, const double* k_sim, float tau, float theta,
+                     uint8_t* mask, int32_t* lut, int32_t* cnt, double* shat,
+                     cudaStream_t stream) {
+  const int T_m = (s.N + s.bq - 1) / s.bq;
+  const int T_n = (s.N + s.bk - 1) / s.bk;
+  const size_t smem_g = sizeof(double) * 2 * kTile * (D + 4);
+  cudaError_t e = cudaFuncSetAttribute(k_shat_dmma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_g));
+  if (e != cudaSuccess) return e;
+  dim3 g1((T_n + kTile - 1) / kTile, (T_m + kTile - 1) / kTile, s.B * s.Hq);
+  k_shat_dmma<D><<<g1, kGemmThreads, smem_g, stream>>>(q_pooled, k_pooled, s.Hq, s.Hkv, T_m, T_n,
+                                                        shat);
+  int sortn = 32;
+  while (sortn < T_n) sortn <<= 1;
+  const size_t smem_r = static_cast<size_t>(kRowWarps) * sortn * 9;
+  e = cudaFuncSetAttribute(k_topcdf_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem_r));
+  if (e != cudaSuccess) return e;
+  const int rows = s.B * s.Hq * T_m;
+  k_topcdf_rows<<<(rows + kRowWarps - 1) / kRowWarps, kRowWarps * 32, smem_r, stream>>>(
+      shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, sortn, s.bq, s.bk, s.causal,
+      static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+size_t predict_workspace_bytes(const sparge_shape& s) {
+  const size_t T_m = (s.N + s.bq - 1) / s.bq;
+  const size_t T_n = (s.N + s.bk - 1) / s.bk;
+  return sizeof(double) * static_cast<size_t>(s.B) * s.Hq * T_m * T_n;
+}
 
 cudaError_t launch_predict(const sparge_shape& s, const double* q_pooled, const double* q_sim,
                            const double* k_pooled, const double* k_sim, float tau, float theta,
-                           uint8_t* mask, int32_t* lut, int32_t* cnt, cudaStream_t stream) {
-  const int T_m = (s.N + s.bq - 1) / s.bq;
-  const int T_n = (s.N + s.bk - 1) / s.bk;
-  int sortn = 32;
-  while (sortn < T_n) sortn <<= 1;
-  dim3 grid((T_m + kRows - 1) / kRows, s.Hq, s.B);
-  if (s.d == 128) {
-    const size_t smem = PredSmem<128>::bytes(sortn);
-    cudaFuncSetAttribute(k_predict_topcdf<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    k_predict_topcdf<128><<<grid, kThreads, smem, stream>>>(
-        q_pooled, q_sim, k_pooled, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, sortn, s.bq, s.bk,
-        s.causal, static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
-  } else {
-    const size_t smem = PredSmem<64>::bytes(sortn);
-    cudaFuncSetAttribute(k_predict_topcdf<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    k_predict_topcdf<64><<<grid, kThreads, smem, stream>>>(
-        q_pooled, q_sim, k_pooled, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, sortn, s.bq, s.bk,
-        s.causal, static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
-  }
-  return cudaGetLastError();
+                           uint8_t* mask, int32_t* lut, int32_t* cnt, void* workspace,
+                           cudaStream_t stream) {
+  double* shat = static_cast<double*>(workspace);
+  if (s.d == 128)
+    return launch_d<128>(s, q_pooled, q_sim, k_pooled, k_sim, tau, theta, mask, lut, cnt, shat,
+                         stream);
+  return launch_d<64>(s, q_pooled, q_sim, k_pooled, k_sim, tau, theta, mask, lut, cnt, shat,
+                      stream);
 }
 
 }  // namespace sparge

@@ -110,17 +110,26 @@ int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_s
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
 }
 
+size_t sparge_predict_workspace(const sparge_shape* shape) {
+  if (!shape_ok(shape)) return 0;
+  return predict_workspace_bytes(*shape);
+}
+
 int sparge_predict_mask(const sparge_shape* shape, const double* q_pooled, const double* q_sim,
                         const double* k_pooled, const double* k_sim, float tau, float theta,
-                        uint8_t* mask, int32_t* lut, int32_t* cnt, void* stream) {
+                        uint8_t* mask, int32_t* lut, int32_t* cnt, void* workspace,
+                        size_t ws_bytes, void* stream) {
   if (!shape_ok(shape) || !q_pooled || !q_sim || !k_pooled || !k_sim || !lut || !cnt)
+    return SPARGE_EINVAL;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u) != 0 ||
+      ws_bytes < predict_workspace_bytes(*shape))
     return SPARGE_EINVAL;
   if (!(tau > 0.f && tau <= 1.f)) return SPARGE_EINVAL;
   if (!(theta >= -1.f && theta <= 1.f)) return SPARGE_EINVAL;
   const int T_n = (shape->N + shape->bk - 1) / shape->bk;
   if (T_n > 2048) return SPARGE_EINVAL;   // one shared-memory row of 2048 (N <= 131072)
   cudaError_t e = launch_predict(*shape, q_pooled, q_sim, k_pooled, k_sim, tau, theta, mask, lut,
-                                 cnt, static_cast<cudaStream_t>(stream));
+                                 cnt, workspace, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
 }
 

@@ -15,7 +15,9 @@ cudaError_t launch_quant(const sparge_shape& s, const void* x, sparge_strides st
 
 cudaError_t launch_predict(const sparge_shape& s, const double* q_pooled, const double* q_sim,
                            const double* k_pooled, const double* k_sim, float tau, float theta,
-                           uint8_t* mask, int32_t* lut, int32_t* cnt, cudaStream_t stream);
+                           uint8_t* mask, int32_t* lut, int32_t* cnt, void* workspace,
+                           cudaStream_t stream);
+size_t predict_workspace_bytes(const sparge_shape& s);
 
 cudaError_t launch_vprep(const sparge_shape& s, const void* v, sparge_strides st,
                          const int32_t* perm, void* vt, int n_pad, cudaStream_t stream);

@@ -53,7 +53,10 @@ _lib.sparge_quantize.argtypes = [ctypes.POINTER(Shape), _vp, Strides, ctypes.c_i
                                  _vp, _vp, _vp, _vp, _vp]
 _lib.sparge_predict_mask.restype = ctypes.c_int
 _lib.sparge_predict_mask.argtypes = [ctypes.POINTER(Shape), _vp, _vp, _vp, _vp,
-                                     ctypes.c_float, ctypes.c_float, _vp, _vp, _vp, _vp]
+                                     ctypes.c_float, ctypes.c_float, _vp, _vp, _vp, _vp,
+                                     ctypes.c_size_t, _vp]
+_lib.sparge_predict_workspace.restype = ctypes.c_size_t
+_lib.sparge_predict_workspace.argtypes = [ctypes.POINTER(Shape)]
 _lib.sparge_attn_workspace.restype = ctypes.c_size_t
 _lib.sparge_attn_workspace.argtypes = [ctypes.POINTER(Shape)]
 _lib.sparge_attn_fwd.restype = ctypes.c_int
@@ -66,6 +69,7 @@ _lib.sparge_attn_status.restype = ctypes.c_int
 _lib.sparge_attn_status.argtypes = [_vp, _vp]
 
 EXPORTED = ("sparge_strerror", "hilbert_permute", "sparge_quantize", "sparge_predict_mask",
+            "sparge_predict_workspace",
             "sparge_attn_workspace", "sparge_attn_fwd", "sparge_attn_fwd_ex",
             "sparge_attn_status")
 SPARGE_ATTN_VPREP_ONLY, SPARGE_ATTN_SKIP_VPREP = 1, 2
@@ -115,11 +119,16 @@ def sparge_quantize(shape, x, is_key, perm, xq, delta, pooled, sim, stream=None)
         _ptr(delta), _ptr(pooled), _ptr(sim), _stream(stream)))
 
 
+def sparge_predict_workspace(shape):
+    return int(_lib.sparge_predict_workspace(ctypes.byref(shape)))
+
+
 def sparge_predict_mask(shape, q_pooled, q_sim, k_pooled, k_sim, tau, theta, mask, lut, cnt,
-                        stream=None):
+                        workspace, stream=None):
     _check("sparge_predict_mask", _lib.sparge_predict_mask(
         ctypes.byref(shape), _ptr(q_pooled), _ptr(q_sim), _ptr(k_pooled), _ptr(k_sim),
-        float(tau), float(theta), _ptr(mask), _ptr(lut), _ptr(cnt), _stream(stream)))
+        float(tau), float(theta), _ptr(mask), _ptr(lut), _ptr(cnt), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream)))
 
 
 def sparge_attn_workspace(shape):
@@ -172,6 +181,8 @@ class Buffers:
         self.counters = torch.zeros(B, Hq, 3, dtype=torch.int64, **kw)
         ws = sparge_attn_workspace(shape)
         self.workspace = torch.zeros((ws + 255) // 256 * 256, dtype=torch.uint8, **kw)
+        pws = sparge_predict_workspace(shape)
+        self.pred_workspace = torch.empty((pws + 255) // 256 * 256, dtype=torch.uint8, **kw)
 
 
 def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=None, out=None,
@@ -190,7 +201,7 @@ def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=No
     sparge_quantize(shape, q, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim, stream)
     sparge_quantize(shape, k, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim, stream)
     sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, tau, theta,
-                        bf.mask, bf.lut, bf.cnt, stream)
+                        bf.mask, bf.lut, bf.cnt, bf.pred_workspace, stream)
     sparge_attn_fwd(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm, o,
                     bf.counters, bf.workspace, stream)
     return o, bf

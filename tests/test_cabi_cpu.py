@@ -47,7 +47,7 @@ def test_strerror_and_validation_without_gpu(sp):
     with pytest.raises(sp.SpargeError):
         sp.hilbert_permute(0, 4, 4)
     rc = sp._lib.sparge_predict_mask(ctypes.byref(good), None, None, None, None, 0.9, 0.5,
-                                     None, None, None, None)
+                                     None, None, None, None, 0, None)
     assert rc == sp.SPARGE_EINVAL
 
 
