@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-f1", action="store_true", help="skip the SpargeAttn+FA2 (bf16 QK) variant")
     ap.add_argument("--profile", action="store_true",
                     help="minimal run for ncu: warmup + steps only, no side legs")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
@@ -195,7 +196,8 @@ def run_ours(args):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step(ev=None, counters=bf.counters, t=tau, th=theta, lm=lam, q_=q, k_=k, v_=v, o_=o):
+    def step(ev=None, counters=bf.counters, t=tau, th=theta, lm=lam, q_=q, k_=k, v_=v, o_=o,
+             shape=shape, bf=bf):
         if ev: ev[0].record()
         sparge.sparge_quantize(shape, q_, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim)
         sparge.sparge_quantize(shape, k_, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim)
@@ -319,6 +321,41 @@ def run_ours(args):
         result["dense"] = {"value": dense_value, "ms_per_step": dms,
                            "speedup": dense_value and value / dense_value,
                            "target_0.8/(1-s)": 0.8 / max(1e-9, 1.0 - sparsity)}
+
+    # ---- f1: the unquantised "SpargeAttn+FA2" kernel (Fig. 7) on the
+    # same inputs and hyper-parameters: bf16 QK^T on the tensor cores ----
+    if not args.no_f1:
+        shape16 = sparge.make_shape(1, Hq, Hkv, N, d, cfg["causal"], q.dtype,
+                                    qk_dtype=sparge.SPARGE_QK_INPUT)
+        bf16b = sparge.Buffers(shape16, device=dev)
+        Kf = min(K, 10)
+        evf = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(Kf)]
+        step(counters=bf16b.counters, shape=shape16, bf=bf16b)
+        sparge.sparge_attn_status(bf16b.workspace)
+        c16 = bf16b.counters.cpu().numpy().astype(np.int64)
+        for s_ in range(Kf):
+            flush.zero_()
+            step(evf[s_], counters=None, shape=shape16, bf=bf16b)
+        torch.cuda.synchronize()
+        stf = np.array([[evf[s_][a].elapsed_time(evf[s_][a + 1]) for a in range(4)]
+                        for s_ in range(Kf)])
+        fms = max_over_ranks(float(stf.sum(1).mean()))
+        f_attn_s = float(stf[:, 3].mean()) * 1e-3
+        qk16 = int(c16[0, :, 0].sum()) * per_tile_qk
+        pv16 = int(c16[0, :, 1].sum()) * per_slice_pv
+        o16 = torch.empty_like(o)
+        step(counters=None, shape=shape16, bf=bf16b, o_=o16)
+        step(counters=None)                  # o = the INT8 path's output again
+        torch.cuda.synchronize()
+        result["f1_fa2_bf16qk"] = {
+            "value": ops_rank * world / (fms * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": fms,
+            "stages_ms": dict(zip(["quant_ms", "predict_ms", "vprep_ms", "attn_ms"],
+                                  stf.mean(0).tolist())),
+            "attn_tensor_frac": (qk16 + pv16) / f_attn_s / 1e12 / bf16_peak,
+            "mask_equal_to_int8": bool(torch.equal(bf16b.mask, bf.mask) and torch.equal(bf16b.cnt, bf.cnt)),
+            "rel_l1_vs_int8_path": float((o16.float() - o.float()).abs().sum() / o.float().abs().sum()),
+        }
+        del bf16b
 
     # ---- e2e through the public API with host buffers ----
     if not args.no_e2e:

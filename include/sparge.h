@@ -45,6 +45,13 @@ enum sparge_status {
 
 enum sparge_dtype { SPARGE_BF16 = 0, SPARGE_FP16 = 1 };
 enum sparge_pv_dtype { SPARGE_PV_SAME_AS_INPUT = 0, SPARGE_PV_FP8_E4M3 = 1 };
+/* Operand type of the QK^T product (stage 2, Alg. 1 line 12):
+ *   SPARGE_QK_INT8   SageAttention per-block INT8 -- the
+ *                    paper's default kernel ("SpargeAttn+SageAttn");
+ *   SPARGE_QK_INPUT  no quantisation: QK^T of the in_dtype values with fp32
+ *                    accumulation -- the paper's "SpargeAttn+FA2" kernel of
+ *                    Fig. 7; scope row f1. */
+enum sparge_qk_dtype { SPARGE_QK_INT8 = 0, SPARGE_QK_INPUT = 1 };
 enum sparge_sim_mode {
   SPARGE_SIM_COSINE = 0,   /* R1-A: mean of the row-normalised Gram matrix  */
   SPARGE_SIM_LITERAL = 1   /* R1-B: mean(X X^T / |max(X X^T)|) on raw rows  */
@@ -60,6 +67,7 @@ typedef struct {
   int pv_dtype;           /* enum sparge_pv_dtype (FP8 -> SPARGE_ENOTIMPL)   */
   int sim_mode;           /* enum sparge_sim_mode                           */
   int smooth_k;           /* 0 only (R14); 1 -> SPARGE_ENOTIMPL              */
+  int qk_dtype;           /* enum sparge_qk_dtype                           */
 } sparge_shape;
 
 /* Human-readable name of a status code (static string, never NULL). */
@@ -91,9 +99,12 @@ int hilbert_permute(int T, int H, int W, int text_prefix,
  *   x      [B, H, N, d] in_dtype, strided by x_str (read-only)
  *   perm   nullable int32 [N]: row r of the (permuted) sequence is x row
  *          perm[r] (the Hilbert gather of §3.7).  NULL = identity.
- *   xq     int8 [B, H, N, d] contiguous, permuted order: per block i,
- *          xq = clamp(rne(fl32(x * fl32(127/amax_i))), -127, 127)  (R11)
- *   delta  fp32 [B, H, T]: fl32(amax_i / 127); 1 for an all-zero block
+ *   xq     [B, H, N, d] contiguous, permuted order.  qk_dtype INT8: int8,
+ *          per block i xq = clamp(rne(fl32(x * fl32(127/amax_i))), -127, 127)
+ *          (R11).  qk_dtype INPUT: in_dtype, the rows of x copied bit for bit
+ *          (the gathered operand of the unquantised f1 kernel).
+ *   delta  fp32 [B, H, T]: fl32(amax_i / 127); 1 for an all-zero block; 1
+ *          everywhere for qk_dtype INPUT
  *   pooled fp64 [B, H, T, d]: mean over the block's valid rows
  *   sim    fp64 [B, H, T]: CosSim of the block per sim_mode     (R1)
  * T = T_m (is_key = 0) or T_n (is_key = 1).
@@ -102,7 +113,7 @@ int hilbert_permute(int T, int H, int W, int text_prefix,
  */
 int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_str,
                     int is_key, const int32_t* perm,
-                    int8_t* xq, float* delta, double* pooled, double* sim,
+                    void* xq, float* delta, double* pooled, double* sim,
                     void* stream);
 
 /*
@@ -149,8 +160,11 @@ size_t sparge_attn_workspace(const sparge_shape* shape);
  * dequantisation (line 12) and the per-warp lambda gate (lines
  * 14-17; §3.4).
  *
- *   qq, dq   int8 [B, Hq, N, d] + fp32 [B, Hq, T_m]  (sparge_quantize of Q)
- *   kq, dk   int8 [B, Hkv, N, d] + fp32 [B, Hkv, T_n] (sparge_quantize of K)
+ *   qq, dq   [B, Hq, N, d] + fp32 [B, Hq, T_m]  (sparge_quantize of Q)
+ *   kq, dk   [B, Hkv, N, d] + fp32 [B, Hkv, T_n] (sparge_quantize of K)
+ *            qq/kq are int8 (qk_dtype INT8: S = (Q^K^^T) dq dk / sqrt(d),
+ *            integer-exact product) or in_dtype (qk_dtype INPUT: S =
+ *            QK^T/sqrt(d) accumulated in fp32 on the tensor cores)
  *   v        [B, Hkv, N, d] in_dtype, strided by v_str, ORIGINAL token order
  *   lut, cnt from sparge_predict_mask
  *   lambda   natural-log units of S = QK^T/sqrt(d) (R3); -INFINITY disables
@@ -171,8 +185,8 @@ size_t sparge_attn_workspace(const sparge_shape* shape);
  * reported by sparge_attn_status.
  */
 int sparge_attn_fwd(const sparge_shape* shape,
-                    const int8_t* qq, const float* dq,
-                    const int8_t* kq, const float* dk,
+                    const void* qq, const float* dq,
+                    const void* kq, const float* dk,
                     const void* v, sparge_strides v_str,
                     const int32_t* lut, const int32_t* cnt,
                     float lambda, const int32_t* perm,
@@ -190,8 +204,8 @@ int sparge_attn_fwd(const sparge_shape* shape,
  * Same arguments, validation and errors as sparge_attn_fwd. */
 enum { SPARGE_ATTN_VPREP_ONLY = 1, SPARGE_ATTN_SKIP_VPREP = 2 };
 int sparge_attn_fwd_ex(const sparge_shape* shape,
-                       const int8_t* qq, const float* dq,
-                       const int8_t* kq, const float* dk,
+                       const void* qq, const float* dq,
+                       const void* kq, const float* dk,
                        const void* v, sparge_strides v_str,
                        const int32_t* lut, const int32_t* cnt,
                        float lambda, const int32_t* perm,
@@ -199,6 +213,21 @@ int sparge_attn_fwd_ex(const sparge_shape* shape,
                        uint64_t* counters,
                        void* workspace, size_t ws_bytes, void* stream,
                        unsigned flags);
+
+/*
+ * sparge_l1_sums -- the accuracy metric of §3.6, relative L1
+ * = sum|O - O'| / sum|O'| (reference in the denominator, R17),
+ * used by the hyper-parameter tuner (scope row f2) and the permutation study
+ * (f3) to score an output against the dense reference on the device.
+ *   o, o_ref  n contiguous 16-bit elements of `dtype` (enum sparge_dtype)
+ *   out       device fp64 [SPARGE_L1_OUT_DOUBLES]: out[0] = sum|o - o_ref|,
+ *             out[1] = sum|o_ref| (fp64 accumulation, deterministic); the
+ *             rest is scratch
+ * Errors: SPARGE_EINVAL (NULL, n < 1, bad dtype, misaligned), SPARGE_ECUDA.
+ */
+#define SPARGE_L1_OUT_DOUBLES 1186
+int sparge_l1_sums(const void* o, const void* o_ref, int dtype, int64_t n, double* out,
+                   void* stream);
 
 /* SYNCHRONISES `stream`, reads and clears the workspace status word:
  * SPARGE_OK, or SPARGE_EINTERNAL if some valid row ended with l = 0. */

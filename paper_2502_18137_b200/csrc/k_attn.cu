@@ -11,31 +11,39 @@
 //        O[I_w] = e^{m - m_new} O[I_w] + P~[I_w] V_j  line 16
 //   O_i = O / l                                       line 19
 //
-// sm_100a design (one CTA per (head, 128-row query tile), 2 CTAs per SM,
-// 256 TMEM columns each: S0 | S1 (int32, 64 cols each) | O (fp32, d cols)):
-//   warp 8    TMA producer: Q^ once, then K^_j (4-stage ring) and V^T_j
-//             (3-stage ring) for every kept j; SWIZZLE_128B/64B tiles.
-//   warp 9    MMA issuer (one thread): tcgen05.mma kind::i8 Q^K^^T -> S[t%2]
-//             then kind::f16 P~ V -> O with P~ read from TMEM (TS form).
-//             QK(t) is issued right after P~V(t-2) (in-order tensor pipe).
-//             The P~V MMA is skipped when all four row groups vote to skip
-//             (their P~ rows are zero otherwise: exact).
-//   warps 0-3 softmax: thread r owns row r == TMEM lane r; warp w is the
-//             gate group I_w (rows 32w..32w+31).  exp2 domain (lambda
-//             compared as lambda*log2e); the gate max is a warp vote
-//             (max_r gap_r > lambda <=> any_r gap_r > lambda); integer row
-//             max; exact int->fp32 via the 1.5*2^23 magic constant folded
-//             into the FFMA bias (R23); packed f32x2 arithmetic; 1 pair in
-//             8 of the exponentials on the FMA pipe (exp2_poly2); P~ (bf16)
-//             written back into the first 32 columns of its own S buffer;
-//             lazy O rescale (R22: the reference max moves only when the
-//             true max grows by > 8 in log2 units; O/l is invariant to the
-//             reference, the gate always uses the true running max).
+// sm_100a design.  A query-tile GROUP = 4 softmax warps + 1 TMA producer
+// warp + 1 MMA warp, 256 TMEM columns (S0 | S1, 64 cols each | O, d cols) and
+// its own K^ / V^T smem rings.  Default: one group per CTA, two CTAs per SM
+// (SPARGE_PAIR=1, an experiment: two groups per CTA, 384 threads, 512 TMEM
+// columns, one CTA per SM).
+//   producer  Q^ once, then K^_j (4-stage ring) and V^T_j (3-stage ring) for
+//             every kept j; SWIZZLE_128B/64B tiles.
+//   MMA       one thread: tcgen05.mma kind::i8 Q^K^^T -> S[t%2] (kind::f16
+//             for the unquantised f1 kernel), then kind::f16 P~ V -> O with
+//             P~ read from TMEM (TS form).  QK(t) is issued right after
+//             P~V(t-2) (in-order tensor pipe).  The P~V MMA is skipped when
+//             all four row groups vote to skip (their P~ rows are zero
+//             otherwise: exact).
+//   softmax   thread r owns row r == TMEM lane r; warp w is the gate group
+//             I_w (rows 32w..32w+31).  exp2 domain (lambda compared as
+//             lambda*log2e); the gate max is a warp vote (max_r gap_r >
+//             lambda <=> any_r gap_r > lambda); integer row max; exact
+//             int->fp32 via the 1.5*2^23 magic constant folded into the FFMA
+//             bias (R23); packed f32x2 arithmetic; 1 pair in 8 of the
+//             exponentials on the FMA pipe (exp2_poly2); P~ (16-bit) written
+//             back into the first 32 columns of its own S buffer; lazy O
+//             rescale (R22: the reference max moves only when the true max
+//             grows by > 8 in log2 units; O/l is invariant to the reference,
+//             the gate always uses the true running max).  With two groups
+//             the exp bursts of the two warps sharing an SMSP alternate
+//             (named-barrier ping-pong), so the MUFU stays busy while the
+//             other warp does its per-tile bookkeeping (measured: no gain).
 //   (profiles/experiments/k_attn_v3_splitrow_speculative.cu: a variant with
 //   rows split over 8 softmax warps -- correct, but slower at 96 registers.)
 #include <cuda.h>
 #include <cstdint>
 #include <climits>
+#include <type_traits>
 
 #include "sm100.cuh"
 #include "sparge_internal.h"
@@ -52,50 +60,66 @@ namespace {
 
 constexpr int BQ = 128;
 constexpr int BK = 64;
-constexpr int KST = 4;        // K^ stages
-constexpr int VST = 3;        // V^T stages
-constexpr int NSOFT = 4;      // softmax warps: one per TMEM lane quadrant
-constexpr int WARP_LOAD = NSOFT, WARP_MMA = NSOFT + 1;
-constexpr int NTHREADS = (NSOFT + 2) * 32;
+constexpr int NSOFT = 4;      // softmax warps per query tile: one per TMEM lane quadrant
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kMagic = 0x4B400000;          // bits of 1.5 * 2^23
 constexpr float kMagicF = 12582912.0f;
-// S pre-bias: the MMA warp fills S with 0x4B400000 (tcgen05.cp from a
-// constant shared-memory tile) before the accumulating INT8 QK MMAs, so the
-// int32 accumulator holds bits(1.5*2^23 + acc) -- the exact fp32 value --
-// and the softmax needs no per-element integer add (kAddMagic = 0).
-// Measured slower (Llama 32K attention 3.93 -> 5.19 ms): the 32 KB
-// smem->TMEM copy per tile occupies the in-order tensor pipe for ~256
-// cycles.  Off by default; kept as a recorded experiment.
-#ifndef SPARGE_S_BIAS
-#define SPARGE_S_BIAS 0
-#endif
-constexpr int kAddMagic = SPARGE_S_BIAS ? 0 : kMagic;
-constexpr int kCBiasBytes = 8192;           // constant tile read by tcgen05.cp
 
 #ifndef SPARGE_POLY_EVERY
 #define SPARGE_POLY_EVERY 8
 #endif
 constexpr int kPolyEvery = SPARGE_POLY_EVERY;   // one pair in kPolyEvery uses exp2_poly2 (0: none)
 
-template <int D>
+// SPARGE_PAIR=1 (experiment, off): one CTA per SM runs two query tiles
+// (NG = 2 groups, each with its own 4 softmax warps, producer warp, MMA warp,
+// smem rings and 256 TMEM columns), optionally with a ping-pong hand-off of
+// the exp bursts between the two warps that share an SMSP (SPARGE_PINGPONG).
+// Measured on Llama 32K: 4.26 ms with ping-pong, 4.23 ms without, vs 3.88 ms
+// for the default of one tile per CTA and two CTAs per SM -- the MUFU
+// contention between co-resident exp bursts is not what limits the softmax.
+#ifndef SPARGE_PAIR
+#define SPARGE_PAIR 0
+#endif
+constexpr bool kPairs = SPARGE_PAIR != 0;
+#ifndef SPARGE_PINGPONG
+#define SPARGE_PINGPONG 1
+#endif
+constexpr bool kPingPong = SPARGE_PINGPONG != 0;
+
+template <int NG>
+struct Roles {
+  static constexpr int SOFT = NSOFT * NG;        // softmax warps 4g .. 4g+3
+  static constexpr int LOAD0 = SOFT;             // TMA producer of group g: LOAD0 + g
+  static constexpr int MMA0 = SOFT + NG;         // MMA issuer of group g: MMA0 + g
+  static constexpr int THREADS = (SOFT + 2 * NG) * 32;
+};
+
+// Shared-memory plan of one query-tile group.  QK16 = the unquantised f1
+// kernel (16-bit Q, K tiles stored as d/64 SWIZZLE_128B K-atoms of 128 B
+// rows); with d = 128 its rings shrink to 2 + 2 stages so that two groups
+// still fit on an SM.
+template <int D, bool QK16>
 struct Smem {
-  static constexpr int Q_BYTES = BQ * D;        // int8
-  static constexpr int K_BYTES = BK * D;        // int8
+  static constexpr int EB = QK16 ? 2 : 1;       // bytes per Q/K element
+  static constexpr int KST = (QK16 && D == 128) ? 2 : 4;   // K stages
+  static constexpr int VST = (QK16 && D == 128) ? 2 : 3;   // V^T stages
+  static constexpr int Q_BYTES = BQ * D * EB;
+  static constexpr int K_BYTES = BK * D * EB;
   static constexpr int V_BYTES = D * BK * 2;    // V^T tile, 16-bit
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * K_BYTES;
   static constexpr int OFF_BAR = OFF_V + VST * V_BYTES;
   static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 3;
-  static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;
-  static constexpr int OFF_XCH = OFF_MISC + 64;             // int [2 bufs][2 halves][BQ]
-  static constexpr int OFF_L = OFF_XCH + 2 * 2 * BQ * 4;   // float [2 halves][BQ]
-  static constexpr int OFF_CB = ((OFF_L + 2 * BQ * 4) + 127) / 128 * 128;   // u32[kCBiasBytes/4]
-  static constexpr int TOTAL = OFF_CB + kCBiasBytes;
-  static constexpr int ALLOC = TOTAL + 1024;     // slack for 1024-B alignment
-  static constexpr int ROW_BYTES_QK = D;          // 128 -> SW128, 64 -> SW64
+  static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;    // [0] TMEM base, [1..8] pv flags
+  static constexpr int TOTAL = OFF_MISC + 64;
+  static constexpr int GROUP = (TOTAL + 1023) / 1024 * 1024;
+  // INT8: one K-atom of D bytes per row (128 -> SW128, 64 -> SW64); 16-bit:
+  // 128-B atoms, the second (d = 128) BQ*128 / BK*128 bytes after the first
+  static constexpr int ROW_BYTES_QK = QK16 ? 128 : D;
+  static constexpr int Q_ATOM = BQ * 128, K_ATOM = BK * 128;
+  static_assert(2 * GROUP + 1024 <= 227 * 1024, "two groups must fit one SM");
 };
 
 struct AttnParams {
@@ -172,42 +196,20 @@ __device__ __forceinline__ uint32_t pack16(float lo, float hi) {
 // the whole tile's exponent of at most 0.75 c, i.e. under one unit of the
 // integer accumulator, far below the INT8 quantisation error in acc (R23).
 // MASKED: INT_MIN entries and rows without a finite reference give 0.
-template <bool MASKED, bool F16>
+// QK16: a holds fp32 S accumulators (no magic constant); masked entries -inf.
+template <bool MASKED, bool F16, bool QK16 = false>
 __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, uint32_t* pw,
                                        float& sum) {
+  constexpr int kAdd = QK16 ? 0 : kMagic;
+  constexpr int kMaskedBits = QK16 ? static_cast<int>(0xFF800000u) : INT_MIN;
   const uint64_t c2 = pk(c, c);
-  const float nbias = fmaf(-kMagicF, c, -m_ref);
+  const float nbias = QK16 ? -m_ref : fmaf(-kMagicF, c, -m_ref);
   const uint64_t nb2 = pk(nbias, nbias);
   const bool row_live = m_ref > -INFINITY;
   uint64_t rs2[2] = {0ull, 0ull};
-#ifdef SPARGE_EXP_PHASED
-  if (!MASKED) {
-    // three explicit phases: all exponent arguments, a burst of independent
-    // MUFU ex2 (plus the FMA-pipe pairs), then sums and packs
-    uint64_t x2[BK / 2];
-#pragma unroll
-    for (int k = 0; k < BK; k += 2)
-      x2[k >> 1] = fma2(pk(__int_as_float(a[k] + kAddMagic), __int_as_float(a[k + 1] + kAddMagic)), c2, nb2);
-#pragma unroll
-    for (int u = 0; u < BK / 2; ++u) {
-      if (kPolyEvery > 0 && (u % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
-        x2[u] = exp2_poly2(x2[u]);
-      else
-        x2[u] = pk(ex2_approx(lo_f(x2[u])), ex2_approx(hi_f(x2[u])));
-    }
-#pragma unroll
-    for (int u = 0; u < BK / 2; ++u) {
-      rs2[u & 1] = add2(rs2[u & 1], x2[u]);
-      pw[u] = pack16<F16>(lo_f(x2[u]), hi_f(x2[u]));
-    }
-    const uint64_t rs = add2(rs2[0], rs2[1]);
-    sum = lo_f(rs) + hi_f(rs);
-    return;
-  }
-#endif
 #pragma unroll
   for (int k = 0; k < BK; k += 2) {
-    const uint64_t x2 = fma2(pk(__int_as_float(a[k] + kAddMagic), __int_as_float(a[k + 1] + kAddMagic)),
+    const uint64_t x2 = fma2(pk(__int_as_float(a[k] + kAdd), __int_as_float(a[k + 1] + kAdd)),
                              c2, nb2);
     uint64_t e2;
     if (!MASKED && kPolyEvery > 0 && ((k >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
@@ -215,8 +217,8 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
     else
       e2 = pk(ex2_approx(lo_f(x2)), ex2_approx(hi_f(x2)));
     if (MASKED) {
-      const float e0 = (a[k] == INT_MIN || !row_live) ? 0.f : lo_f(e2);
-      const float e1 = (a[k + 1] == INT_MIN || !row_live) ? 0.f : hi_f(e2);
+      const float e0 = (a[k] == kMaskedBits || !row_live) ? 0.f : lo_f(e2);
+      const float e1 = (a[k + 1] == kMaskedBits || !row_live) ? 0.f : hi_f(e2);
       e2 = pk(e0, e1);
     }
     rs2[(k >> 1) & 1] = add2(rs2[(k >> 1) & 1], e2);
@@ -226,14 +228,64 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
   sum = lo_f(rs) + hi_f(rs);
 }
 
-template <int D, bool CAUSAL, bool F16>
-__global__ void __launch_bounds__(NTHREADS, 2)
+template <int D, bool CAUSAL, bool F16, bool QK16, int NG>
+__global__ void __launch_bounds__(Roles<NG>::THREADS, 2 / NG)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  using L = Smem<D>;
+  using L = Smem<D, QK16>;
+  using R = Roles<NG>;
+  constexpr int KST = L::KST, VST = L::VST;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
+  unsigned char* smem0 = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const int warp = __shfl_sync(0xffffffffu, warp_id(), 0), lane = lane_id();
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem0 + L::OFF_MISC);   // group 0's
+  const int bhq = blockIdx.y;
+  const int b = bhq / p.Hq, hq = bhq % p.Hq;
+  const int bkv = b * p.Hkv + hq / p.group;
+  // query tile of group gg: u = blockIdx.x * NG + gg in launch order (causal:
+  // longest rows first); u >= T_m (odd T_m, last pair) is an empty group
+  auto tile_of = [&](int gg, int& i_out) -> int {
+    const int u = static_cast<int>(blockIdx.x) * NG + gg;
+    if (u >= p.T_m) { i_out = p.T_m; return 0; }
+    i_out = CAUSAL ? (p.T_m - 1 - u) : u;
+    return p.cnt[static_cast<int64_t>(bhq) * p.T_m + i_out];
+  };
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int gg = 0; gg < NG; ++gg) {
+      uint64_t* bg = reinterpret_cast<uint64_t*>(smem0 + gg * L::GROUP + L::OFF_BAR);
+      mbar_init(bg, 1);                                                  // q_full
+      for (int s = 0; s < KST; ++s) { mbar_init(bg + 1 + s, 1); mbar_init(bg + 1 + KST + s, 1); }
+      for (int s = 0; s < VST; ++s) {
+        mbar_init(bg + 1 + 2 * KST + s, 1);
+        mbar_init(bg + 1 + 2 * KST + VST + s, 1);
+      }
+      uint64_t* sf = bg + 1 + 2 * KST + 2 * VST;
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(sf + s, 1);            // s_full
+        mbar_init(sf + 2 + s, NSOFT);    // p_full
+        mbar_init(sf + 4 + s, 1);        // o_done
+      }
+    }
+    fence_mbar_init();
+  }
+  if (warp == R::MMA0) tmem_alloc<256 * NG>(tmem_base_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  // group of this warp: softmax warps 4g..4g+3, producer LOAD0+g, MMA MMA0+g.
+  // `warp` comes from a shuffle, so the compiler treats it (and g, and every
+  // smem / barrier / TMEM address derived from it) as warp-uniform; one copy
+  // of the code serves both groups (two copies thrash the instruction cache).
+  const int g = (NG == 1) ? 0
+                          : (warp < R::SOFT ? (warp >> 2)
+                                            : (warp < R::MMA0 ? warp - R::LOAD0 : warp - R::MMA0));
+  unsigned char* smem = smem0 + g * L::GROUP;
   int8_t* sQ = reinterpret_cast<int8_t*>(smem + L::OFF_Q);
   int8_t* sK = reinterpret_cast<int8_t*>(smem + L::OFF_K);
   unsigned char* sV = smem + L::OFF_V;
@@ -246,76 +298,54 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   uint64_t* s_full = v_empty + VST;
   uint64_t* p_full = s_full + 2;
   uint64_t* o_done = p_full + 2;
-  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
-  uint32_t* tmem_base_slot = misc;           // [0]
-  uint32_t* pv_flag = misc + 1;              // [2][4]
-
-  const int warp = warp_id(), lane = lane_id();
-  const int i = CAUSAL ? (p.T_m - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
-  const int bhq = blockIdx.y;
-  const int b = bhq / p.Hq, hq = bhq % p.Hq;
-  const int bkv = b * p.Hkv + hq / p.group;
-  const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + i;
-  const int n_tiles = p.cnt[row_id];
+  uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC) + 1;       // [2][4]
+  int i = 0, i_other = 0;
+  const int n_tiles = tile_of(g, i);
+  const int n_other = (NG == 2) ? tile_of(g ^ 1, i_other) : 0;
+  const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + min(i, p.T_m - 1);
   const int32_t* lut_row = p.lut + row_id * p.T_n;
+  const uint32_t tS0 = tmem_base + g * 256, tO = tS0 + 128;
 
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < KST; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
-    for (int s = 0; s < VST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(s_full + s, 1);
-      mbar_init(p_full + s, NSOFT);
-      mbar_init(o_done + s, 1);
-    }
-    fence_mbar_init();
-  }
-  if (SPARGE_S_BIAS) {
-    uint4* cb = reinterpret_cast<uint4*>(smem + L::OFF_CB);
-    for (int e = threadIdx.x; e < kCBiasBytes / 16; e += NTHREADS)
-      cb[e] = make_uint4(kMagic, kMagic, kMagic, kMagic);
-    fence_proxy_async_smem();     // generic writes -> tcgen05.cp (async proxy)
-  }
-  if (warp == WARP_MMA) tmem_alloc<256>(tmem_base_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_base_slot;
-  const uint32_t tS0 = tmem, tO = tmem + 128;
-
-  if (warp == WARP_LOAD) {
+  if (warp >= R::LOAD0 && warp < R::MMA0) {
     // ============================ TMA producer ============================
-    if (lane == 0) {
+    if (lane == 0 && n_tiles > 0) {
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       mbar_arrive_expect_tx(q_full, L::Q_BYTES);
-      tma_load_3d(sQ, &tmQ, q_full, 0, i * BQ, bhq);
-      int j_next = n_tiles > 0 ? __ldg(lut_row) : 0;
+      if (QK16) {
+#pragma unroll
+        for (int h = 0; h < D / 64; ++h) tma_load_3d(sQ + h * L::Q_ATOM, &tmQ, q_full, h * 64, i * BQ, bhq);
+      } else {
+        tma_load_3d(sQ, &tmQ, q_full, 0, i * BQ, bhq);
+      }
+      int j_next = __ldg(lut_row);
       for (int t = 0; t < n_tiles; ++t) {
         const int j = j_next;
         if (t + 1 < n_tiles) j_next = __ldg(lut_row + t + 1);
         const int ks = t % KST;
         mbar_wait(k_empty + ks, ((t / KST) & 1) ^ 1);
         mbar_arrive_expect_tx(k_full + ks, L::K_BYTES);
-        tma_load_3d(sK + ks * L::K_BYTES, &tmK, k_full + ks, 0, j * BK, bkv);
+        if (QK16) {
+#pragma unroll
+          for (int h = 0; h < D / 64; ++h)
+            tma_load_3d(sK + ks * L::K_BYTES + h * L::K_ATOM, &tmK, k_full + ks, h * 64, j * BK, bkv);
+        } else {
+          tma_load_3d(sK + ks * L::K_BYTES, &tmK, k_full + ks, 0, j * BK, bkv);
+        }
         const int vs = t % VST;
         mbar_wait(v_empty + vs, ((t / VST) & 1) ^ 1);
         mbar_arrive_expect_tx(v_full + vs, L::V_BYTES);
         tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
       }
     }
-  } else if (warp == WARP_MMA) {
+  } else if (warp >= R::MMA0) {
     // ============================ MMA issuer ==============================
-    if (lane == 0) {
-      constexpr uint32_t IDESC_QK = idesc_i8(BQ, BK);
+    if (lane == 0 && n_tiles > 0) {
+      constexpr uint32_t IDESC_QK =
+          QK16 ? (F16 ? idesc_f16(BQ, BK) : idesc_bf16(BQ, BK)) : idesc_i8(BQ, BK);
       constexpr uint32_t IDESC_PV = F16 ? idesc_f16(BQ, D) : idesc_bf16(BQ, D);
       const uint64_t dQ = umma_desc_kmajor(smem_u32(sQ), L::ROW_BYTES_QK);
-      // no-swizzle descriptor over the constant tile (LBO 128 B, SBO 256 B;
-      // every byte it can address holds the bias pattern)
-      const uint64_t cb_desc = static_cast<uint64_t>((smem_u32(smem + L::OFF_CB) >> 4) & 0x3FFFu) |
-                               (static_cast<uint64_t>(128 >> 4) << 16) |
-                               (static_cast<uint64_t>(256 >> 4) << 32) | (1ull << 46);
       unsigned long long issued = 0;
       mbar_wait(q_full, 0);
       tc_fence_after();
@@ -328,7 +358,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
                           pv_flag[pb * 4 + 2] | pv_flag[pb * 4 + 3]) != 0;
         if (any) {
           const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
-          const uint32_t tP = tS0 + pb * BK;     // P~ bf16, 32 packed columns
+          const uint32_t tP = tS0 + pb * BK;     // P~ 16-bit, 32 packed columns
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
             mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
@@ -346,32 +376,34 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         // reading S(t-2) before they arrived on p_full(t-2)).
         tc_fence_after();
         const uint64_t dK = umma_desc_kmajor(smem_u32(sK + ks * L::K_BYTES), L::ROW_BYTES_QK);
-        if (SPARGE_S_BIAS) {
-          // S[sb] = 0x4B400000 everywhere (8 x 128 lanes x 8 columns), in
-          // tensor-pipe order after P~V(t-2) and before QK(t)
+        if (QK16) {
+          // K = 16 per kind::f16 MMA (32 B): 4 steps per 128-B atom, then
+          // the next atom (fp32 S accumulators)
 #pragma unroll
-          for (int cc = 0; cc < BK / 8; ++cc)
-            asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;"
-                         ::"r"(tS0 + sb * BK + 8 * cc), "l"(cb_desc) : "memory");
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_f16(tS0 + sb * BK, dQ + (((kk >> 2) * L::Q_ATOM + (kk & 3) * 32) >> 4),
+                    dK + (((kk >> 2) * L::K_ATOM + (kk & 3) * 32) >> 4), IDESC_QK, kk > 0 ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < D / 32; ++kk)       // K = 32 per kind::i8 MMA (32 B)
+            mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, kk > 0 ? 1u : 0u);
         }
-#pragma unroll
-        for (int kk = 0; kk < D / 32; ++kk)       // K = 32 per kind::i8 MMA (32 B)
-          mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK,
-                 (SPARGE_S_BIAS || kk > 0) ? 1u : 0u);
         tc_commit(s_full + sb);
         tc_commit(k_empty + ks);
         if (t > 0) do_pv(t - 1);
       }
-      if (n_tiles > 0) do_pv(n_tiles - 1);
+      do_pv(n_tiles - 1);
       if (p.counters) atomicAdd(p.counters + bhq * 3 + 2, issued);
     }
   } else {
     // ============================ softmax warps ===========================
-    const int r = threadIdx.x;                 // row within the tile == TMEM lane
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const int quad = warp & 3;                 // TMEM lane quadrant = gate group I_w
+    const int r = quad * 32 + lane;            // row within the tile == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
     const int row_g = i * BQ + r;
     const bool row_valid = row_g < p.N;
     const bool tile_tail = (i * BQ + BQ > p.N);
+    constexpr int kMaskedBits = QK16 ? static_cast<int>(0xFF800000u) : INT_MIN;   // -inf / INT_MIN
     {
       uint32_t z[32];
 #pragma unroll
@@ -394,121 +426,166 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       cj = __ldg(lut_row + lane);
       cc_ = dq_scale * __ldg(dk_row + cj);
     }
+    // Pair mode (NG = 2): the exp phases of the two warps that share an SMSP
+    // (warp quad of group 0 and of group 1) alternate strictly -- a bar.sync
+    // / bar.arrive hand-off on barriers 1+quad+4g -- so one warp's MUFU burst
+    // overlaps the other's per-tile bookkeeping instead of contending for the
+    // same MUFU.  Both run max(n_0, n_1) hand-off rounds (a finished group
+    // keeps passing the token), group 1 starts by handing the token to group 0.
+    const uint32_t my_bar = 1 + quad + 4 * g, other_bar = 1 + quad + 4 * (g ^ 1);
+    constexpr bool PP = NG == 2 && kPingPong;
+    const int n_iter = PP ? max(n_tiles, n_other) : n_tiles;
+    if (PP && g == 1 && n_iter > 0) named_bar_arrive(other_bar, 64);
 #ifdef SPARGE_PHASE_TIMING
     long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
     long long ph_last = clock64();
 #endif
     for (int t = 0; t < n_tiles; ++t) {
-      const int tl = t & 31;
-      if (tl == 0) {
-        if (t > 0) { cj = nj; cc_ = dq_scale * ndk; }
-        if (t + 32 + lane < n_tiles) nj = __ldg(lut_row + t + 32 + lane);
-      } else if (tl == 16) {
-        if (t + 16 + lane < n_tiles) ndk = __ldg(dk_row + nj);
-      }
-      const int j = __shfl_sync(0xffffffffu, cj, tl);
-      const float c = __shfl_sync(0xffffffffu, cc_, tl);
       const int sb = t & 1;
       const uint32_t tS = tS0 + sb * BK + lane_base;
-
-      PT_MARK(0);
-      mbar_wait(s_full + sb, (t >> 1) & 1);
-      PT_MARK(1);
-      tc_fence_after();
       int32_t a[BK];
-      tmem_ld32(tS, reinterpret_cast<uint32_t*>(a));
-      tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(a) + 32);
-      tmem_wait_ld();
-      PT_MARK(6);
-
-      // ---- masking of boundary tiles: keys >= N, causal keys > query, rows >= N
-      const int k0 = j * BK;
-      const bool need_mask = tile_tail || (k0 + BK > p.N) || (CAUSAL && (k0 + BK - 1 > i * BQ));
-      if (need_mask) {
-        const int kmax = CAUSAL ? min(p.N - 1, row_g) : p.N - 1;
-#pragma unroll
-        for (int k = 0; k < BK; ++k)
-          if (!row_valid || k0 + k > kmax) a[k] = INT_MIN;
-      }
-      // integer-domain row max (monotone: the dequant scale c > 0), eight
-      // independent chains
-      int m8[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) m8[u] = max(a[u], a[u + 8]);
-#pragma unroll
-      for (int k = 16; k < BK; k += 16)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) m8[u] = max(m8[u], max(a[k + u], a[k + 8 + u]));
-      const int mx = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])),
-                         max(max(m8[4], m8[5]), max(m8[6], m8[7])));
-      // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32 through
-      // the magic constant (I2F runs on the slow XU pipe)
-      const float m_loc = (mx == INT_MIN) ? -INFINITY
-                                          : (__int_as_float(mx + kAddMagic) - kMagicF) * c;
-      const float m_new = fmaxf(m_true, m_loc);
-      // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
-      const bool compute = __any_sync(0xffffffffu, (mx != INT_MIN) && (m_loc - m_new > p.lam2));
-      // lazy rescale (R22): move the reference max only when it lags the
-      // true max by more than the threshold (always when it is -inf)
-      const bool need = compute && (m_new > m_ref + kRescaleThreshold);
-      const bool rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
+      float c = 0.f;
+      bool need_mask = false, compute = false, need = false, rescale_o = false;
       float alpha = 1.f;
-      if (need) {
-        alpha = ex2_approx(m_ref - m_new);   // 0 when m_ref = -inf (l, O are 0 then)
-        l *= alpha;
-        m_ref = m_new;
-      }
-      m_true = m_new;
-      PT_MARK(2);
-
-      // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ into TMEM ----
-      uint32_t pw[BK / 2];
-      float rsum;
-      if (need_mask) exps64<true, F16>(a, c, m_ref, pw, rsum);
-      else exps64<false, F16>(a, c, m_ref, pw, rsum);
-      l += rsum;           // R9: skipped groups still add their mass to l
-      if (!compute) {
-#pragma unroll
-        for (int k = 0; k < BK / 2; ++k) pw[k] = 0u;
-      }
-      PT_MARK(4);
-
-      if (rescale_o) {
-        // O rows of this warp hold P~V of earlier tiles: wait for the last
-        // issued P~V, then rescale in TMEM (before p_full(t) releases P~V(t)).
-        if (t >= 1) mbar_wait(o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
-          uint32_t ov[32];
-          tmem_ld32(tO + lane_base + cc * 32, ov);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
-          tmem_st32(tO + lane_base + cc * 32, ov);
+      {
+        const int tl = t & 31;
+        if (tl == 0) {
+          if (t > 0) { cj = nj; cc_ = dq_scale * ndk; }
+          if (t + 32 + lane < n_tiles) nj = __ldg(lut_row + t + 32 + lane);
+        } else if (tl == 16) {
+          if (t + 16 + lane < n_tiles) ndk = __ldg(dk_row + nj);
         }
-      }
-      PT_MARK(3);
+        const int j = __shfl_sync(0xffffffffu, cj, tl);
+        c = __shfl_sync(0xffffffffu, cc_, tl);
 
-      // P~(t) overwrites the first 32 columns of S[sb]: S(t) is already in
-      // registers, and QK(t) -- complete, per s_full -- executed after
-      // P~V(t-2), the previous reader of this buffer.
-      tmem_st32(tS, pw);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + warp)),
-                     "r"(compute ? 1u : 0u) : "memory");
-        mbar_arrive(p_full + sb);
+        PT_MARK(0);
+        mbar_wait(s_full + sb, (t >> 1) & 1);
+        PT_MARK(1);
+        tc_fence_after();
+        tmem_ld32(tS, reinterpret_cast<uint32_t*>(a));
+        tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(a) + 32);
+        tmem_wait_ld();
+        PT_MARK(6);
+
+        // ---- masking of boundary tiles: keys >= N, causal keys > query, rows >= N
+        const int k0 = j * BK;
+        need_mask = tile_tail || (k0 + BK > p.N) || (CAUSAL && (k0 + BK - 1 > i * BQ));
+        if (need_mask) {
+          const int kmax = CAUSAL ? min(p.N - 1, row_g) : p.N - 1;
+#pragma unroll
+          for (int k = 0; k < BK; ++k)
+            if (!row_valid || k0 + k > kmax) a[k] = kMaskedBits;
+        }
+        float m_loc;
+        bool row_has;
+        if (QK16) {
+          // fp32 row max of S (masked entries -inf), eight chains
+          const float* af = reinterpret_cast<const float*>(a);
+          float f8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f8[u] = fmaxf(af[u], af[u + 8]);
+#pragma unroll
+          for (int k = 16; k < BK; k += 16)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) f8[u] = fmaxf(f8[u], fmaxf(af[k + u], af[k + 8 + u]));
+          const float mxf = fmaxf(fmaxf(fmaxf(f8[0], f8[1]), fmaxf(f8[2], f8[3])),
+                                  fmaxf(fmaxf(f8[4], f8[5]), fmaxf(f8[6], f8[7])));
+          row_has = mxf > -INFINITY;
+          m_loc = row_has ? mxf * c : -INFINITY;
+        } else {
+          // integer-domain row max (monotone: the dequant scale c > 0), eight
+          // independent chains
+          int m8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) m8[u] = max(a[u], a[u + 8]);
+#pragma unroll
+          for (int k = 16; k < BK; k += 16)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) m8[u] = max(m8[u], max(a[k + u], a[k + 8 + u]));
+          const int mx = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])),
+                             max(max(m8[4], m8[5]), max(m8[6], m8[7])));
+          // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32
+          // through the magic constant (I2F runs on the slow XU pipe)
+          row_has = mx != INT_MIN;
+          m_loc = row_has ? (__int_as_float(mx + kMagic) - kMagicF) * c : -INFINITY;
+        }
+        const float m_new = fmaxf(m_true, m_loc);
+        // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
+        compute = __any_sync(0xffffffffu, row_has && (m_loc - m_new > p.lam2));
+        // lazy rescale (R22): move the reference max only when it lags the
+        // true max by more than the threshold (always when it is -inf)
+        need = compute && (m_new > m_ref + kRescaleThreshold);
+        rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
+        if (need) {
+          alpha = ex2_approx(m_ref - m_new);   // 0 when m_ref = -inf (l, O are 0 then)
+          l *= alpha;
+          m_ref = m_new;
+        }
+        m_true = m_new;
+        PT_MARK(2);
       }
-      if (compute) ++slices;
-      PT_MARK(5);
+
+      if (PP) named_bar_sync(my_bar, 64);
+      // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ ----
+      uint32_t pw[BK / 2];
+      {
+        float rsum;
+        if (need_mask) exps64<true, F16, QK16>(a, c, m_ref, pw, rsum);
+        else exps64<false, F16, QK16>(a, c, m_ref, pw, rsum);
+        l += rsum;           // R9: skipped groups still add their mass to l
+      }
+      if (PP && !(g == 1 && t == n_iter - 1)) named_bar_arrive(other_bar, 64);
+
+      {
+        if (!compute) {
+#pragma unroll
+          for (int k = 0; k < BK / 2; ++k) pw[k] = 0u;
+        }
+        PT_MARK(4);
+
+        if (rescale_o) {
+          // O rows of this warp hold P~V of earlier tiles: wait for the last
+          // issued P~V, then rescale in TMEM (before p_full(t) releases P~V(t)).
+          if (t >= 1) mbar_wait(o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t ov[32];
+            tmem_ld32(tO + lane_base + cc * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
+            tmem_st32(tO + lane_base + cc * 32, ov);
+          }
+        }
+        PT_MARK(3);
+
+        // P~(t) overwrites the first 32 columns of S[sb]: S(t) is already in
+        // registers, and QK(t) -- complete, per s_full -- executed after
+        // P~V(t-2), the previous reader of this buffer.
+        tmem_st32(tS, pw);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + quad)),
+                       "r"(compute ? 1u : 0u) : "memory");
+          mbar_arrive(p_full + sb);
+        }
+        if (compute) ++slices;
+        PT_MARK(5);
+      }
+    }
+    // this group is done: keep passing the token while the other one works
+    for (int t = n_tiles; PP && t < n_iter; ++t) {
+      named_bar_sync(my_bar, 64);
+      if (!(g == 1 && t == n_iter - 1)) named_bar_arrive(other_bar, 64);
     }
 #ifdef SPARGE_PHASE_TIMING
     if (lane == 0 && p.phase_clk)
       for (int k = 0; k < 7; ++k) atomicAdd(p.phase_clk + k, static_cast<unsigned long long>(ph[k]));
-    if (threadIdx.x == 0 && p.phase_clk) atomicAdd(p.phase_clk + 7, static_cast<unsigned long long>(n_tiles));
+    if (quad == 0 && lane == 0 && p.phase_clk)
+      atomicAdd(p.phase_clk + 7, static_cast<unsigned long long>(n_tiles));
 #endif
 
     // ---- epilogue: O_i = O / l (line 19), scattered back through perm ----
@@ -538,27 +615,29 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     }
     if (p.counters) {
       if (lane == 0) atomicAdd(p.counters + bhq * 3 + 1, static_cast<unsigned long long>(slices));
-      if (threadIdx.x == 0) atomicAdd(p.counters + bhq * 3 + 0, static_cast<unsigned long long>(n_tiles));
+      if (quad == 0 && lane == 0)
+        atomicAdd(p.counters + bhq * 3 + 0, static_cast<unsigned long long>(n_tiles));
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == WARP_MMA) {
+  if (warp == R::MMA0) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<256 * NG>(tmem_base);
   }
 }
 
-template <int D, bool CAUSAL, bool F16>
+template <int D, bool CAUSAL, bool F16, bool QK16>
 cudaError_t launch_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                      const AttnParams& p, int B, cudaStream_t stream) {
-  auto kern = k_sparse_attn<D, CAUSAL, F16>;
-  const int smem = Smem<D>::ALLOC;
+  constexpr int NG = kPairs ? 2 : 1;
+  auto kern = k_sparse_attn<D, CAUSAL, F16, QK16, NG>;
+  const int smem = NG * Smem<D, QK16>::GROUP + 1024;   // + slack for 1024-B alignment
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(p.T_m, B * p.Hq);
-  kern<<<grid, NTHREADS, smem, stream>>>(mq, mk, mv, p);
+  dim3 grid((p.T_m + NG - 1) / NG, B * p.Hq);
+  kern<<<grid, Roles<NG>::THREADS, smem, stream>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
 
@@ -583,7 +662,10 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
   p.Hq = s.Hq; p.Hkv = s.Hkv; p.group = s.Hq / s.Hkv;
   p.phase_clk = reinterpret_cast<unsigned long long*>(status + 8);   // debug builds only
   const bool f16 = s.in_dtype == SPARGE_FP16;
-#define SPARGE_A(D, C, F) return launch_t<D, C, F>(mq, mk, mv, p, s.B, stream)
+  const bool qk16 = s.qk_dtype == SPARGE_QK_INPUT;
+#define SPARGE_A(D, C, F)                                                      \
+  return qk16 ? launch_t<D, C, F, true>(mq, mk, mv, p, s.B, stream)            \
+              : launch_t<D, C, F, false>(mq, mk, mv, p, s.B, stream)
   if (s.d == 128) {
     if (s.causal) { if (f16) SPARGE_A(128, true, true); else SPARGE_A(128, true, false); }
     else          { if (f16) SPARGE_A(128, false, true); else SPARGE_A(128, false, false); }
@@ -594,6 +676,10 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
 #undef SPARGE_A
 }
 
-int attn_smem_bytes(int d) { return d == 128 ? Smem<128>::ALLOC : Smem<64>::ALLOC; }
+int attn_smem_bytes(int d, int qk16) {
+  const int ng = kPairs ? 2 : 1;
+  if (qk16) return ng * (d == 128 ? Smem<128, true>::GROUP : Smem<64, true>::GROUP) + 1024;
+  return ng * (d == 128 ? Smem<128, false>::GROUP : Smem<64, false>::GROUP) + 1024;
+}
 
 }  // namespace sparge

@@ -27,6 +27,7 @@ bool shape_ok(const sparge_shape* s) {
   if (s->in_dtype != SPARGE_BF16 && s->in_dtype != SPARGE_FP16) return false;
   if (s->sim_mode != SPARGE_SIM_COSINE && s->sim_mode != SPARGE_SIM_LITERAL) return false;
   if (s->pv_dtype != SPARGE_PV_SAME_AS_INPUT && s->pv_dtype != SPARGE_PV_FP8_E4M3) return false;
+  if (s->qk_dtype != SPARGE_QK_INT8 && s->qk_dtype != SPARGE_QK_INPUT) return false;
   return true;
 }
 
@@ -99,7 +100,7 @@ int hilbert_permute(int T, int H, int W, int text_prefix, int32_t* perm_host,
 }
 
 int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_str, int is_key,
-                    const int32_t* perm, int8_t* xq, float* delta, double* pooled, double* sim,
+                    const int32_t* perm, void* xq, float* delta, double* pooled, double* sim,
                     void* stream) {
   if (!shape_ok(shape) || !x || !xq || !delta || !pooled || !sim) return SPARGE_EINVAL;
   if (!strides_ok(x_str) || !aligned16(x) || !aligned16(xq)) return SPARGE_EINVAL;
@@ -139,8 +140,8 @@ size_t sparge_attn_workspace(const sparge_shape* shape) {
   return kStatusBytes + vt;
 }
 
-int sparge_attn_fwd(const sparge_shape* shape, const int8_t* qq, const float* dq,
-                    const int8_t* kq, const float* dk, const void* v, sparge_strides v_str,
+int sparge_attn_fwd(const sparge_shape* shape, const void* qq, const float* dq,
+                    const void* kq, const float* dk, const void* v, sparge_strides v_str,
                     const int32_t* lut, const int32_t* cnt, float lambda, const int32_t* perm,
                     void* o, sparge_strides o_str, uint64_t* counters, void* workspace,
                     size_t ws_bytes, void* stream) {
@@ -148,8 +149,8 @@ int sparge_attn_fwd(const sparge_shape* shape, const int8_t* qq, const float* dq
                             counters, workspace, ws_bytes, stream, 0u);
 }
 
-int sparge_attn_fwd_ex(const sparge_shape* shape, const int8_t* qq, const float* dq,
-                       const int8_t* kq, const float* dk, const void* v, sparge_strides v_str,
+int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* dq,
+                       const void* kq, const float* dk, const void* v, sparge_strides v_str,
                        const int32_t* lut, const int32_t* cnt, float lambda,
                        const int32_t* perm, void* o, sparge_strides o_str, uint64_t* counters,
                        void* workspace, size_t ws_bytes, void* stream, unsigned flags) {
@@ -179,24 +180,40 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const int8_t* qq, const float*
   }
   if (flags & SPARGE_ATTN_VPREP_ONLY) return SPARGE_OK;
 
+  // Q and K operand maps.  INT8: one box of d bytes per row (SWIZZLE_128B at
+  // d=128, 64B at d=64).  16-bit (qk_dtype INPUT): boxes of 64 elements =
+  // 128 B per row, loaded d/64 times (one SWIZZLE_128B K-atom each).
+  const bool qk16 = s.qk_dtype == SPARGE_QK_INPUT;
+  const CUtensorMapDataType dt16 =
+      s.in_dtype == SPARGE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const CUtensorMapSwizzle sw_qk =
-      s.d == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+      (qk16 || s.d == 128) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const CUtensorMapDataType dt_qk = qk16 ? dt16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  const uint64_t eb = qk16 ? 2 : 1;
+  const uint32_t box0 = qk16 ? 64u : static_cast<uint32_t>(s.d);
   CUtensorMap mq, mk, mv;
   const uint64_t d = static_cast<uint64_t>(s.d);
   const uint64_t N = static_cast<uint64_t>(s.N);
-  if (!encode3d(&mq, CU_TENSOR_MAP_DATA_TYPE_UINT8, qq, d, N,
-                static_cast<uint64_t>(s.B) * s.Hq, d, d * N, s.d, 128, sw_qk) ||
-      !encode3d(&mk, CU_TENSOR_MAP_DATA_TYPE_UINT8, kq, d, N,
-                static_cast<uint64_t>(s.B) * s.Hkv, d, d * N, s.d, 64, sw_qk) ||
-      !encode3d(&mv,
-                s.in_dtype == SPARGE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
-                                          : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
-                vt, static_cast<uint64_t>(n_pad), d, static_cast<uint64_t>(s.B) * s.Hkv,
+  if (!encode3d(&mq, dt_qk, qq, d, N, static_cast<uint64_t>(s.B) * s.Hq, d * eb, d * N * eb,
+                box0, 128, sw_qk) ||
+      !encode3d(&mk, dt_qk, kq, d, N, static_cast<uint64_t>(s.B) * s.Hkv, d * eb, d * N * eb,
+                box0, 64, sw_qk) ||
+      !encode3d(&mv, dt16, vt, static_cast<uint64_t>(n_pad), d, static_cast<uint64_t>(s.B) * s.Hkv,
                 static_cast<uint64_t>(n_pad) * 2, d * n_pad * 2, 64, s.d,
                 CU_TENSOR_MAP_SWIZZLE_128B))
     return SPARGE_ECUDA;
 
   e = launch_attn(s, mq, mk, mv, dq, dk, lut, cnt, lambda, perm, o, o_str, counters, status, st);
+  return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
+}
+
+int sparge_l1_sums(const void* o, const void* o_ref, int dtype, int64_t n, double* out,
+                   void* stream) {
+  if (!o || !o_ref || !out || n < 1) return SPARGE_EINVAL;
+  if (dtype != SPARGE_BF16 && dtype != SPARGE_FP16) return SPARGE_EINVAL;
+  if (!aligned16(o) || !aligned16(o_ref) || (reinterpret_cast<uintptr_t>(out) & 7u)) return SPARGE_EINVAL;
+  cudaError_t e = launch_l1_sums(o, o_ref, dtype == SPARGE_FP16, n, out,
+                                 static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
 }
 

@@ -10,7 +10,7 @@
 namespace sparge {
 
 cudaError_t launch_quant(const sparge_shape& s, const void* x, sparge_strides st, int is_key,
-                         const int32_t* perm, int8_t* xq, float* delta, double* pooled,
+                         const int32_t* perm, void* xq, float* delta, double* pooled,
                          double* sim, cudaStream_t stream);
 
 cudaError_t launch_predict(const sparge_shape& s, const double* q_pooled, const double* q_sim,
@@ -28,7 +28,11 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
                         const int32_t* perm, void* o, sparge_strides o_str,
                         uint64_t* counters, unsigned int* status, cudaStream_t stream);
 
-int attn_smem_bytes(int d);
+int attn_smem_bytes(int d, int qk16);
+
+constexpr int kL1Blocks = (SPARGE_L1_OUT_DOUBLES - 2) / 2;
+cudaError_t launch_l1_sums(const void* o, const void* o_ref, int f16, int64_t n, double* out,
+                           cudaStream_t stream);
 
 int hilbert_build(int T, int H, int W, int text_prefix, int32_t* perm, int32_t* inv);
 

@@ -19,6 +19,8 @@ LIB_PATH = os.path.join(_HERE, os.environ.get("SPARGE_LIB", "libsparge.so"))
 SPARGE_OK, SPARGE_EINVAL, SPARGE_EINTERNAL, SPARGE_ECUDA, SPARGE_ENOTIMPL = 0, 2, 3, 4, 5
 SPARGE_BF16, SPARGE_FP16 = 0, 1
 SPARGE_SIM_COSINE, SPARGE_SIM_LITERAL = 0, 1
+# QK^T operand: INT8 (SageAttention, the default) or the input dtype ("SpargeAttn+FA2", row f1)
+SPARGE_QK_INT8, SPARGE_QK_INPUT = 0, 1
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2502_18137_b200.build` "
@@ -40,7 +42,7 @@ class Strides(ctypes.Structure):
 class Shape(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int) for f in
                 ("B", "Hq", "Hkv", "N", "d", "bq", "bk", "cw", "causal", "in_dtype",
-                 "pv_dtype", "sim_mode", "smooth_k")]
+                 "pv_dtype", "sim_mode", "smooth_k", "qk_dtype")]
 
 
 _vp, _i32p, _f32p, _f64p, _u8p, _u64p, _i8p = (ctypes.c_void_p,) * 7
@@ -65,13 +67,16 @@ _lib.sparge_attn_fwd.argtypes = [ctypes.POINTER(Shape), _vp, _vp, _vp, _vp, _vp,
                                  ctypes.c_size_t, _vp]
 _lib.sparge_attn_fwd_ex.restype = ctypes.c_int
 _lib.sparge_attn_fwd_ex.argtypes = _lib.sparge_attn_fwd.argtypes + [ctypes.c_uint]
+_lib.sparge_l1_sums.restype = ctypes.c_int
+_lib.sparge_l1_sums.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int64, _vp, _vp]
+SPARGE_L1_OUT_DOUBLES = 1186
 _lib.sparge_attn_status.restype = ctypes.c_int
 _lib.sparge_attn_status.argtypes = [_vp, _vp]
 
 EXPORTED = ("sparge_strerror", "hilbert_permute", "sparge_quantize", "sparge_predict_mask",
             "sparge_predict_workspace",
             "sparge_attn_workspace", "sparge_attn_fwd", "sparge_attn_fwd_ex",
-            "sparge_attn_status")
+            "sparge_attn_status", "sparge_l1_sums")
 SPARGE_ATTN_VPREP_ONLY, SPARGE_ATTN_SKIP_VPREP = 1, 2
 
 
@@ -96,9 +101,11 @@ def _strides(t):
     return Strides(t.stride(0), t.stride(1), t.stride(2))
 
 
-def make_shape(B, Hq, Hkv, N, d, causal=False, dtype=torch.bfloat16, sim_mode=SPARGE_SIM_COSINE):
+def make_shape(B, Hq, Hkv, N, d, causal=False, dtype=torch.bfloat16, sim_mode=SPARGE_SIM_COSINE,
+               qk_dtype=SPARGE_QK_INT8):
     return Shape(B, Hq, Hkv, N, d, 128, 64, 4, int(bool(causal)),
-                 SPARGE_FP16 if dtype == torch.float16 else SPARGE_BF16, 0, sim_mode, 0)
+                 SPARGE_FP16 if dtype == torch.float16 else SPARGE_BF16, 0, sim_mode, 0,
+                 int(qk_dtype))
 
 
 # ------------------------------------------------------------------ C-ABI calls
@@ -152,6 +159,28 @@ def sparge_attn_fwd_ex(shape, qq, dq, kq, dk, v, lut, cnt, lam, perm, o, counter
         int(flags)))
 
 
+def sparge_l1_sums(o, o_ref, out=None, stream=None):
+    """Device relative-L1 sums of two same-shape contiguous bf16/fp16 tensors
+    (§3.6).  Returns the device fp64 buffer; out[0] = sum|o - o_ref|,
+    out[1] = sum|o_ref|."""
+    if o.shape != o_ref.shape or o.dtype != o_ref.dtype:
+        raise ValueError("o and o_ref must have the same shape and dtype")
+    if not (o.is_contiguous() and o_ref.is_contiguous()):
+        raise ValueError("o and o_ref must be contiguous")
+    if out is None:
+        out = torch.empty(SPARGE_L1_OUT_DOUBLES, dtype=torch.float64, device=o.device)
+    _check("sparge_l1_sums", _lib.sparge_l1_sums(
+        _ptr(o), _ptr(o_ref), SPARGE_FP16 if o.dtype == torch.float16 else SPARGE_BF16,
+        o.numel(), _ptr(out), _stream(stream)))
+    return out
+
+
+def relative_l1(o, o_ref, stream=None):
+    """sum|o - o_ref| / sum|o_ref| computed by the library kernel (host float)."""
+    s = sparge_l1_sums(o, o_ref, stream=stream)[:2].cpu()
+    return float(s[0] / s[1])
+
+
 def sparge_attn_status(workspace, stream=None):
     """Synchronises the stream; raises SpargeError(SPARGE_EINTERNAL) if a valid
     row ended with l = 0."""
@@ -167,8 +196,12 @@ class Buffers:
         tm, tn = math.ceil(N / 128), math.ceil(N / 64)
         kw = dict(device=device)
         self.shape = shape
-        self.qq = torch.empty(B, Hq, N, d, dtype=torch.int8, **kw)
-        self.kq = torch.empty(B, Hkv, N, d, dtype=torch.int8, **kw)
+        if shape.qk_dtype == SPARGE_QK_INPUT:
+            qk_t = torch.float16 if shape.in_dtype == SPARGE_FP16 else torch.bfloat16
+        else:
+            qk_t = torch.int8
+        self.qq = torch.empty(B, Hq, N, d, dtype=qk_t, **kw)
+        self.kq = torch.empty(B, Hkv, N, d, dtype=qk_t, **kw)
         self.dq = torch.empty(B, Hq, tm, dtype=torch.float32, **kw)
         self.dk = torch.empty(B, Hkv, tn, dtype=torch.float32, **kw)
         self.q_pooled = torch.empty(B, Hq, tm, d, dtype=torch.float64, **kw)
@@ -186,14 +219,15 @@ class Buffers:
 
 
 def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=None, out=None,
-                   sim_mode=SPARGE_SIM_COSINE, stream=None):
+                   sim_mode=SPARGE_SIM_COSINE, stream=None, qk_dtype=SPARGE_QK_INT8):
     """The whole hot path (a1 quantise Q, K -> a2 predict -> a3 attention) on
     device tensors q [B,Hq,N,d], k/v [B,Hkv,N,d] (bf16 or fp16).  perm: optional
     int32 device tensor [N] (Hilbert order); O is returned in original order.
+    qk_dtype=SPARGE_QK_INPUT selects the unquantised "SpargeAttn+FA2" kernel.
     Returns (O, buffers)."""
     B, Hq, N, d = q.shape
     Hkv = k.shape[1]
-    shape = make_shape(B, Hq, Hkv, N, d, causal, q.dtype, sim_mode)
+    shape = make_shape(B, Hq, Hkv, N, d, causal, q.dtype, sim_mode, qk_dtype)
     if buffers is None:
         buffers = Buffers(shape, device=q.device)
     bf = buffers
@@ -219,7 +253,7 @@ class HostPipeline:
     copies and streams (torch)."""
 
     def __init__(self, B, Hq, Hkv, N, d, causal=False, dtype=torch.bfloat16, chunks=4,
-                 device="cuda", sim_mode=SPARGE_SIM_COSINE):
+                 device="cuda", sim_mode=SPARGE_SIM_COSINE, qk_dtype=SPARGE_QK_INT8):
         if Hkv % chunks:
             chunks = 1
         self.B, self.Hq, self.Hkv, self.N, self.d = B, Hq, Hkv, N, d
@@ -227,7 +261,7 @@ class HostPipeline:
         self.chunks = chunks
         self.kv_per = Hkv // chunks
         self.q_per = self.kv_per * self.group
-        self.shape = make_shape(B, self.q_per, self.kv_per, N, d, causal, dtype, sim_mode)
+        self.shape = make_shape(B, self.q_per, self.kv_per, N, d, causal, dtype, sim_mode, qk_dtype)
         kw = dict(device=device, dtype=dtype)
         self.q = torch.empty(B, Hq, N, d, **kw)
         self.k = torch.empty(B, Hkv, N, d, **kw)
@@ -260,7 +294,8 @@ class HostPipeline:
                 self.s_comp.wait_event(ev_in)
                 sparge_forward(self.q[:, qs], self.k[:, ks], self.v[:, ks], tau, theta, lam,
                                causal=bool(self.shape.causal), perm=perm, buffers=bf,
-                               out=self.o[:, qs], stream=self.s_comp)
+                               out=self.o[:, qs], stream=self.s_comp,
+                               qk_dtype=self.shape.qk_dtype)
                 ev_out = torch.cuda.Event()
                 ev_out.record(self.s_comp)
             with torch.cuda.stream(self.s_d2h):

@@ -1,0 +1,160 @@
+"""§3.6 hyper-parameter determination on the GPU path -- scope row f2.
+
+"We first conduct a grid search for tau and theta to identify the optimal pair
+that maximizes sparsity while ensuring L1 < l_1.  Subsequently, we perform
+another grid search for lambda to find the optimal value that further
+maximizes sparsity while maintaining L1 < l_2."
+
+Readings (R24-R26):
+  * one (tau, theta, lambda) per layer, shared by all heads ("for each
+    attention layer");
+  * stage 1 runs with lambda = -inf (the lambda filter off); the L1 of a
+    candidate is the MAX over the calibration inputs ("constrain the attention
+    error across five different model inputs"), its sparsity the MEAN;
+  * ties go to the safer value: larger tau, then larger theta; larger |lambda|;
+  * the dense reference O' is full attention without quantisation -- the
+    f1 kernel (bf16 QK^T) with tau = 1, theta = -1, lambda = -inf (the paper
+    scores against FlashAttention2);
+  * no feasible (tau, theta) -> the dense configuration (1, -1, -inf), flagged.
+
+The selection logic (`select_stage1`, `select_stage2`, `tune_layer`) is pure
+host code over an evaluator callback, so it is testable on the CPU; the
+`GpuEvaluator` runs every candidate through the C-ABI kernels (a1 once per
+input, a2 + a3 per candidate, L1 by `sparge_l1_sums`).
+"""
+
+import math
+
+DEFAULT_TAU_GRID = (0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.98, 1.0)
+DEFAULT_THETA_GRID = (-1.0, 0.0, 0.2, 0.4, 0.6, 0.8)          # -1 = judge off
+DEFAULT_LAMBDA_GRID = (-math.inf, -20.0, -15.0, -10.0, -8.0, -6.0, -5.0, -4.0)
+
+# (l1, l2) per model family
+PAPER_BOUNDS = {"llama": (0.08, 0.09), "cogvideox": (0.05, 0.06), "mochi": (0.05, 0.06),
+                "sd35": (0.07, 0.08), "flux": (0.07, 0.08), "open_sora_plan": (0.03, 0.035)}
+
+
+def select_stage1(rows, l1):
+    """rows: iterable of (tau, theta, l1_max, sparsity).  The feasible row
+    (l1_max < l1) of maximal sparsity; ties -> larger tau, then larger theta.
+    None if nothing is feasible."""
+    best = None
+    for tau, theta, err, sp in rows:
+        if not err < l1:
+            continue
+        key = (sp, tau, theta)
+        if best is None or key > best[0]:
+            best = (key, (tau, theta, err, sp))
+    return None if best is None else best[1]
+
+
+def select_stage2(rows, l2):
+    """rows: iterable of (lam, l1_max, sparsity).  The feasible row of maximal
+    sparsity; ties -> the more negative lambda.  None if nothing is feasible."""
+    best = None
+    for lam, err, sp in rows:
+        if not err < l2:
+            continue
+        key = (sp, -lam)
+        if best is None or key > best[0]:
+            best = (key, (lam, err, sp))
+    return None if best is None else best[1]
+
+
+def tune_layer(evaluate, l1, l2, tau_grid=DEFAULT_TAU_GRID, theta_grid=DEFAULT_THETA_GRID,
+               lambda_grid=DEFAULT_LAMBDA_GRID):
+    """Two-stage grid search of §3.6.  evaluate(tau, theta, lam) -> (l1_max,
+    mean sparsity) over the calibration set.  Returns a dict with the chosen
+    values, the achieved stage-1 / stage-2 L1 and sparsity, and both scans."""
+    if not (0 < l1 < l2):
+        raise ValueError("need 0 < l1 < l2")
+    if not tau_grid or not theta_grid or not lambda_grid:
+        raise ValueError("empty grid")
+    if any(not (0 < t <= 1) for t in tau_grid) or any(not (lm < 0) for lm in lambda_grid):
+        raise ValueError("tau in (0, 1], lambda < 0")
+    scan1 = []
+    for tau in tau_grid:
+        for theta in theta_grid:
+            err, sp = evaluate(tau, theta, -math.inf)
+            scan1.append((tau, theta, err, sp))
+    pick = select_stage1(scan1, l1)
+    if pick is None:
+        err, sp = evaluate(1.0, -1.0, -math.inf)
+        return {"tau": 1.0, "theta": -1.0, "lambda": -math.inf, "fallback": True,
+                "l1_stage1": err, "l1_stage2": err, "sparsity_stage1": sp, "sparsity": sp,
+                "scan_stage1": scan1, "scan_stage2": []}
+    tau, theta, err1, sp1 = pick
+    scan2 = []
+    for lam in lambda_grid:
+        err, sp = evaluate(tau, theta, lam)
+        scan2.append((lam, err, sp))
+    pick2 = select_stage2(scan2, l2)
+    if pick2 is None:                      # lambda = -inf is feasible whenever l2 > err1
+        pick2 = (-math.inf, err1, sp1)
+    lam, err2, sp2 = pick2
+    return {"tau": tau, "theta": theta, "lambda": lam, "fallback": False,
+            "l1_stage1": err1, "l1_stage2": err2, "sparsity_stage1": sp1, "sparsity": sp2,
+            "scan_stage1": scan1, "scan_stage2": scan2}
+
+
+def live_tiles(N, causal, bq=128, bk=64):
+    """Live (b_q x b_k) tiles of one head (reading R8)."""
+    tm, tn = -(-N // bq), -(-N // bk)
+    if not causal:
+        return tm * tn
+    return sum(min(tn, (min((i + 1) * bq, N) - 1) // bk + 1) for i in range(tm))
+
+
+class GpuEvaluator:
+    """Scores (tau, theta, lambda) on a calibration set through the C-ABI path.
+
+    inputs: list of (q, k, v) device tensors [B, H, N, d] (same shape);
+    perm: optional int32 device permutation (Hilbert order).  a1 runs once per
+    input; each candidate reruns a2 (prediction) and a3 (attention)."""
+
+    def __init__(self, inputs, causal=False, perm=None):
+        import torch
+        from . import sparge
+        self.sp, self.torch = sparge, torch
+        q0, k0, _ = inputs[0]
+        B, Hq, N, d = q0.shape
+        Hkv = k0.shape[1]
+        self.causal, self.perm = causal, perm
+        self.shape = sparge.make_shape(B, Hq, Hkv, N, d, causal, q0.dtype)
+        self.live = live_tiles(N, causal) * B * Hq
+        self.items = []
+        self.evals = 0
+        # dense reference O' per input: f1 kernel (no quantisation), filters off
+        shape16 = sparge.make_shape(B, Hq, Hkv, N, d, causal, q0.dtype,
+                                    qk_dtype=sparge.SPARGE_QK_INPUT)
+        b16 = sparge.Buffers(shape16, device=q0.device, with_mask=False)
+        for q, k, v in inputs:
+            ref = torch.empty_like(q)
+            sparge.sparge_forward(q, k, v, 1.0, -1.0, -math.inf, causal=causal, perm=perm,
+                                  buffers=b16, out=ref, qk_dtype=sparge.SPARGE_QK_INPUT)
+            bf = sparge.Buffers(self.shape, device=q.device, with_mask=False)
+            sparge.sparge_quantize(self.shape, q, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim)
+            sparge.sparge_quantize(self.shape, k, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim)
+            self.items.append((v, ref, bf, torch.empty_like(q)))
+        del b16
+        torch.cuda.synchronize()
+
+    def __call__(self, tau, theta, lam):
+        sp, torch = self.sp, self.torch
+        errs, sparsities = [], []
+        for v, ref, bf, o in self.items:
+            bf.counters.zero_()
+            sp.sparge_predict_mask(self.shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, tau,
+                                   theta, None, bf.lut, bf.cnt, bf.pred_workspace)
+            sp.sparge_attn_fwd(self.shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam,
+                               self.perm, o, bf.counters, bf.workspace)
+            errs.append(sp.sparge_l1_sums(o, ref))
+            sparsities.append(bf.counters.sum(dim=(0, 1)))
+        torch.cuda.synchronize()
+        self.evals += 1
+        err = max(float(e[0] / e[1]) for e in (x[:2].cpu() for x in errs))
+        sps = []
+        for c in sparsities:
+            qk, pv = int(c[0]), int(c[1])
+            sps.append(1.0 - (qk + pv / 4.0) / (2.0 * self.live))
+        return err, sum(sps) / len(sps)

@@ -3,7 +3,7 @@ library (SPARGE_PHASE_TIMING) and print the per-phase cycle split of the
 softmax warps.  GPU only.  usage: python scripts/phase_timing.py [workload]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["SPARGE_LIB"] = "libsparge_sparge_phase_timing.so"
+os.environ.setdefault("SPARGE_LIB", "libsparge_sparge_phase_timing.so")
 import numpy as np, torch
 import bench
 from paper_2502_18137_b200 import inputs, sparge
@@ -21,9 +21,9 @@ torch.cuda.synchronize()
 ph = bf.workspace[32:32 + 64].view(torch.int64).cpu().numpy()
 tiles = ph[7]
 order = [(0, "loop top (LUT chunk, shfl)"), (1, "wait s_full (QK done)"), (6, "LDTM S + wait::ld"),
-         (2, "mask + half max + publish"), (4, "speculative exp2 + row sum"),
-         (3, "bar.sync + gate + (rare) rescale"), (5, "P~ STTM + fence + arrive")]
+         (2, "mask + row max + gate votes"), (4, "[pair: bar.sync] exp2 + row sum"),
+         (3, "(rare) O rescale"), (5, "P~ STTM + fence + arrive")]
 tot = ph[:7].sum()
-print(f"{w}: tiles {tiles}, cycles per tile per softmax warp {tot / tiles / 8:.0f}")
+print(f"{os.environ['SPARGE_LIB']} {w}: tiles {tiles}, cycles per tile per softmax warp {tot / tiles / 4:.0f}")
 for k, n in order:
-    print(f"  {n:36s} {ph[k] / tiles / 8:8.0f} cyc  {100 * ph[k] / tot:5.1f}%")
+    print(f"  {n:36s} {ph[k] / tiles / 4:8.0f} cyc  {100 * ph[k] / tot:5.1f}%")

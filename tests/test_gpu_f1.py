@@ -1,0 +1,144 @@
+"""Scope row f1: the "SpargeAttn+FA2" kernel configuration (Fig. 7, P:L526,
+P:L533) -- the same stage-1 masks and lambda gate with QK^T in the input dtype
+(bf16/fp16 tensor cores, fp32 accumulation) instead of per-block INT8.
+
+Parity against the oracle's quantise-off mode (`spargeattn_head(quantize=
+False)`: S = QK^T/sqrt(d) in fp64 on the bf16 inputs):
+  * the a1 copy is the (permuted) input bit for bit, delta = 1, and the
+    stage-1 statistics equal the INT8 mode's (prediction never sees the
+    quantised values);
+  * masks bit-exact except near-threshold blocks; QK tile counters exact;
+  * O within relative L1 2e-2 (asserted < 5e-3 as the bug signal).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import bf16_np, oracle_forward, rel_l1
+from paper_2502_18137_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+BUG_L1 = 5e-3
+
+
+def _dev(x, dtype=torch.bfloat16):
+    return inputs.to_device(x, dtype)
+
+
+def _run(lib, q, k, v, tau, theta, lam, causal, perm=None):
+    pt = None if perm is None else torch.from_numpy(perm.astype(np.int32)).cuda()
+    o, bf = lib.sparge_forward(q, k, v, tau, theta, lam, causal=causal, perm=pt,
+                               qk_dtype=lib.SPARGE_QK_INPUT)
+    lib.sparge_attn_status(bf.workspace)
+    return o, bf
+
+
+def _check_masks(gpu_mask, ref, label):
+    bad = (gpu_mask != ref["M"]) & ~ref["near"]
+    assert not bad.any(), f"{label}: {int(bad.sum())} mask mismatches outside near-threshold"
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("d,is_key,N", [(128, 0, 1000), (64, 1, 77), (128, 1, 256)])
+def test_copy_mode_quantize(lib, dtype, d, is_key, N):
+    x = _dev(inputs.gaussian(N + d, 1, 2, N, d, scale=2.0), dtype)
+    perm = np.random.default_rng(N).permutation(N).astype(np.int32)
+    pt = torch.from_numpy(perm).cuda()
+    H = 2
+    bs = 64 if is_key else 128
+    T = math.ceil(N / bs)
+    outs = {}
+    for mode in (lib.SPARGE_QK_INT8, lib.SPARGE_QK_INPUT):
+        shape = lib.make_shape(1, H, H if is_key else 1, N, d, False, dtype, qk_dtype=mode)
+        xq = torch.empty(1, H, N, d, dtype=torch.int8 if mode == 0 else dtype, device="cuda")
+        dl = torch.empty(1, H, T, dtype=torch.float32, device="cuda")
+        po = torch.empty(1, H, T, d, dtype=torch.float64, device="cuda")
+        si = torch.empty(1, H, T, dtype=torch.float64, device="cuda")
+        lib.sparge_quantize(shape, x, is_key, pt, xq, dl, po, si)
+        torch.cuda.synchronize()
+        outs[mode] = (xq.cpu(), dl.cpu(), po.cpu(), si.cpu())
+    xq, dl, po, si = outs[lib.SPARGE_QK_INPUT]
+    assert torch.equal(xq.view(torch.int16), x.cpu()[:, :, torch.from_numpy(perm).long()].view(torch.int16))
+    assert (dl == 1.0).all()
+    assert torch.equal(po, outs[0][2]) and torch.equal(si, outs[0][3])
+
+
+def test_c1_planted_f1(lib):
+    q, k, v = (_dev(a) for a in inputs.planted(0))
+    o, bf = _run(lib, q, k, v, 0.9, 0.5, -5.0, False)
+    ref = oracle_forward(bf16_np(q)[0], bf16_np(k)[0], bf16_np(v)[0], 0.9, 0.5, -5.0,
+                         quantize=False)[0]
+    _check_masks(bf.mask.cpu().numpy()[0, 0], ref, "C1")
+    err = rel_l1(bf16_np(o)[0, 0], ref["o"])
+    assert err < BUG_L1, err
+    cnt = bf.counters.cpu().numpy()[0, 0]
+    assert cnt[0] == ref["cnt"]["qk"]
+    assert abs(int(cnt[1]) - ref["cnt"]["pv_slices"]) <= 2
+
+
+@pytest.mark.parametrize("N,d,Hq,Hkv,causal", [
+    (1000, 128, 4, 2, True), (1000, 64, 2, 2, False), (777, 128, 2, 1, False),
+    (2048, 128, 4, 1, True), (130, 64, 1, 1, True),
+])
+def test_f1_ragged(lib, N, d, Hq, Hkv, causal):
+    qn, kn, vn = inputs.llm_local(N + d + 7, N, d=d, Hq=Hq, Hkv=Hkv, gamma=1.5)
+    q, k, v = _dev(qn), _dev(kn), _dev(vn)
+    o, bf = _run(lib, q, k, v, 0.9, 0.5, -5.0, causal)
+    ref = oracle_forward(bf16_np(q)[0], bf16_np(k)[0], bf16_np(v)[0], 0.9, 0.5, -5.0,
+                         causal=causal, group=Hq // Hkv, quantize=False)
+    gm = bf.mask.cpu().numpy()[0]
+    og = bf16_np(o)[0]
+    cnt = bf.counters.cpu().numpy()[0]
+    for h in range(Hq):
+        _check_masks(gm[h], ref[h], f"head {h}")
+        err = rel_l1(og[h], ref[h]["o"])
+        assert err < BUG_L1, (h, err)
+        assert cnt[h, 0] == ref[h]["cnt"]["qk"]
+
+
+def test_f1_filters_off_equals_dense(lib):
+    """P1 on the f1 kernel: tau=1, theta=-1, lambda=-inf is plain dense
+    attention on the bf16 inputs (no quantisation anywhere)."""
+    N, d = 900, 128
+    qn, kn, vn = (inputs.gaussian(s, 1, 2, N, d) for s in (1, 2, 3))
+    q, k, v = _dev(qn), _dev(kn), _dev(vn)
+    o, bf = _run(lib, q, k, v, 1.0, -1.0, -math.inf, False)
+    qs, ks, vs = bf16_np(q)[0], bf16_np(k)[0], bf16_np(v)[0]
+    for h in range(2):
+        ref = O.dense_attention(qs[h], ks[h], vs[h])
+        assert rel_l1(bf16_np(o)[0, h], ref) < BUG_L1
+    assert (bf.mask.cpu().numpy() == 1).all()
+
+
+def test_f1_hilbert_fp16(lib):
+    T, H, W, pre, d = 3, 10, 12, 40, 64
+    qn, kn, vn = inputs.video(5, T, H, W, d=d, heads=2, text_prefix=pre)
+    perm, _ = lib.hilbert_permute(T, H, W, pre)
+    q, k, v = (_dev(a, torch.float16) for a in (qn, kn, vn))
+    o, bf = _run(lib, q, k, v, 0.9, 0.5, -5.0, False, perm=perm)
+    ref = oracle_forward(bf16_np(q)[0], bf16_np(k)[0], bf16_np(v)[0], 0.9, 0.5, -5.0,
+                         perm=perm.astype(np.int64), quantize=False)
+    gm = bf.mask.cpu().numpy()[0]
+    for h in range(2):
+        _check_masks(gm[h], ref[h], f"head {h}")
+        assert rel_l1(bf16_np(o)[0, h], ref[h]["o"]) < BUG_L1
+
+
+def test_f1_masks_equal_int8_masks(lib):
+    """Stage 1 is independent of the QK^T operand type: identical LUTs."""
+    N, d, Hq, Hkv = 3000, 128, 4, 2
+    qn, kn, vn = inputs.llm_local(11, N, d=d, Hq=Hq, Hkv=Hkv)
+    q, k, v = _dev(qn), _dev(kn), _dev(vn)
+    _, b8 = lib.sparge_forward(q, k, v, 0.9, 0.5, -5.0, causal=True)
+    _, b16 = _run(lib, q, k, v, 0.9, 0.5, -5.0, True)
+    assert torch.equal(b8.mask, b16.mask) and torch.equal(b8.cnt, b16.cnt)
+    lut8, lut16, cnt = b8.lut.cpu().numpy(), b16.lut.cpu().numpy(), b8.cnt.cpu().numpy()
+    for h in range(Hq):
+        for i in range(cnt.shape[2]):
+            c = cnt[0, h, i]
+            assert np.array_equal(lut8[0, h, i, :c], lut16[0, h, i, :c])
