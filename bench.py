@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--profile", action="store_true",
                     help="minimal run for ncu: warmup + steps only, no side legs")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
+    ap.add_argument("--tau", type=float, default=None, help="override tau (default 0.9, R20)")
+    ap.add_argument("--theta", type=float, default=None, help="override theta (default 0.5)")
+    ap.add_argument("--lam", type=float, default=None, help="override lambda (default -5)")
     return ap.parse_args()
 
 
@@ -182,6 +185,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = workload_cfg(args.workload)
+    for key in ("tau", "theta", "lam"):
+        if getattr(args, key) is not None:
+            cfg[key] = getattr(args, key)
     N, d, Hq, Hkv = cfg["N"], cfg["d"], cfg["Hq"], cfg["Hkv"]
     tau, theta, lam = cfg["tau"], cfg["theta"], cfg["lam"]
 
@@ -465,6 +471,9 @@ def run_reference(args):
         return
     import oracle as O
     cfg = workload_cfg(args.workload)
+    for key in ("tau", "theta", "lam"):
+        if getattr(args, key) is not None:
+            cfg[key] = getattr(args, key)
     N, d = cfg["N"], cfg["d"]
     tm = math.ceil(N / 128)
     qn, kn, vn = gen_inputs(cfg, seed=1000, heads=[0])

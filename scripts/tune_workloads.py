@@ -1,0 +1,52 @@
+"""Scope row f2: run the §3.6 tuner on the GPU path for the
+BASELINE workloads at the paper's (l1, l2) bounds and write
+profiles/<name>.json.  Five seeded calibration inputs per workload ("five
+different model inputs"), full size.  GPU only.
+
+usage: python scripts/tune_workloads.py [--out profiles/r01_f2_tuned.json] [workload ...]
+"""
+import argparse, json, math, os, sys, time
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import bench
+from paper_2502_18137_b200 import inputs, tuner
+
+BOUNDS = {"llama31_8b_32k": tuner.PAPER_BOUNDS["llama"], "cogvideox_2b": tuner.PAPER_BOUNDS["cogvideox"],
+          "mochi": tuner.PAPER_BOUNDS["mochi"], "sweep_32k": tuner.PAPER_BOUNDS["llama"],
+          "sweep_128k": tuner.PAPER_BOUNDS["llama"]}
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_f2_tuned.json"))
+ap.add_argument("workloads", nargs="*", default=["llama31_8b_32k", "cogvideox_2b", "mochi"])
+args = ap.parse_args()
+report = {}
+for w in args.workloads:
+    cfg = bench.workload_cfg(w)
+    l1, l2 = BOUNDS[w]
+    t0 = time.time()
+    cal = [tuple(inputs.to_device(a) for a in bench.gen_inputs(cfg, 2000 + s)) for s in range(5)]
+    perm_np = bench.hilbert_perm(cfg)
+    perm = None if perm_np is None else torch.from_numpy(perm_np).cuda()
+    t1 = time.time()
+    ev = tuner.GpuEvaluator(cal, causal=cfg["causal"], perm=perm)
+    fixed = ev(cfg["tau"], cfg["theta"], cfg["lam"])
+    t2 = time.time()
+    res = tuner.tune_layer(ev, l1, l2)
+    t3 = time.time()
+    out = {k: v for k, v in res.items() if not k.startswith("scan")}
+    out.update({"l1_bound": l1, "l2_bound": l2, "evaluations": ev.evals, "calibration_inputs": 5,
+                "tune_seconds": round(t3 - t2, 2), "input_gen_seconds": round(t1 - t0, 1),
+                "fixed_R20": {"tau": cfg["tau"], "theta": cfg["theta"], "lambda": cfg["lam"],
+                              "l1": fixed[0], "sparsity": fixed[1]},
+                "scan_stage1": [list(r) for r in res["scan_stage1"]],
+                "scan_stage2": [[r[0] if math.isfinite(r[0]) else "-inf", r[1], r[2]]
+                                for r in res["scan_stage2"]]})
+    if not math.isfinite(out["lambda"]):
+        out["lambda"] = "-inf"
+    report[w] = out
+    print(w, json.dumps({k: v for k, v in out.items() if not k.startswith("scan")}), flush=True)
+    del ev, cal
+    torch.cuda.empty_cache()
+os.makedirs(os.path.dirname(args.out), exist_ok=True)
+json.dump(report, open(args.out, "w"), indent=1, default=str)
