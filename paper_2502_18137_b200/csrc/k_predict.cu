@@ -154,7 +154,104 @@ __device__ __forceinline__ void sort_desc(uint64_t* key, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(kRowWarps * 32)
+// Register bitonic sort, descending, of SORTN = 32*R 64-bit keys held
+// lane-major (rank i = lane*R + r): stages with partner distance jj < R are
+// compare-exchanges between two registers of one lane, stages with jj >= R
+// exchange register r with lane ^ (jj/R) by shuffle (15 of the 55 stages at
+// SORTN = 1024).  No shared memory, no bank conflicts.
+template <int R, int JJ>
+__device__ __forceinline__ void reg_stage_c(uint64_t (&v)[R], int k, int lane) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if ((r & JJ) == 0) {
+      const int i = lane * R + r;
+      const bool desc = (i & k) == 0;
+      const uint64_t a = v[r], b = v[r + JJ];
+      const bool sw = desc ? (b > a) : (a > b);
+      v[r] = sw ? b : a;
+      v[r + JJ] = sw ? a : b;
+    }
+  }
+}
+template <int R>
+__device__ __forceinline__ void reg_stage(uint64_t (&v)[R], int jj, int k, int lane) {
+  if (R > 1 && jj == 1) reg_stage_c<R, (R > 1 ? 1 : 0)>(v, k, lane);
+  if (R > 2 && jj == 2) reg_stage_c<R, (R > 2 ? 2 : 0)>(v, k, lane);
+  if (R > 4 && jj == 4) reg_stage_c<R, (R > 4 ? 4 : 0)>(v, k, lane);
+  if (R > 8 && jj == 8) reg_stage_c<R, (R > 8 ? 8 : 0)>(v, k, lane);
+  if (R > 16 && jj == 16) reg_stage_c<R, (R > 16 ? 16 : 0)>(v, k, lane);
+}
+template <int R>
+__device__ __forceinline__ void lane_stage(uint64_t (&v)[R], int ld, int k, int lane) {
+  const bool lower = (lane & ld) == 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], ld);
+    const bool desc = ((lane * R + r) & k) == 0;
+    const bool take_max = (lower == desc);
+    const bool o_bigger = o > v[r];
+    v[r] = (take_max == o_bigger) ? o : v[r];
+  }
+}
+template <int R>
+__device__ __forceinline__ void sort_desc_reg(uint64_t (&v)[R], int lane) {
+#pragma unroll 1
+  for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll 1
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj >= R) lane_stage<R>(v, jj / R, k, lane);
+      else reg_stage<R>(v, jj, k, lane);
+    }
+  }
+}
+
+// padded shared-memory index of entry j (one 8-B pad per 32 entries) so the
+// lane-major reads lane*R + r hit distinct banks
+__device__ __forceinline__ int pidx(int j) { return j + (j >> 5); }
+
+// TopCdf of one row with the register sort: keys (padded layout) in smem ->
+// registers (lane-major), sort, lane-local sequential prefix sums + a warp
+// scan of the lane totals, flags by rank.
+template <int R>
+__device__ __forceinline__ void topcdf_reg(uint64_t* ukey, uint8_t* flag, int T_n, double tau,
+                                           int lane) {
+  uint64_t v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = ukey[pidx(lane * R + r)];
+  sort_desc_reg<R>(v, lane);
+  // c_k = (exclusive prefix of the lane totals) + lane-local sequential sum;
+  // recomputed identically in each pass (deterministic), so no array of c
+  auto p_of = [&](int r) {
+    return (lane * R + r < T_n) ? __longlong_as_double(v[r] & ~0x7FFull) : 0.0;
+  };
+  double tot = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) tot += p_of(r);
+  const double off = warp_incl_scan(tot, lane) - tot;
+  double acc = off, cmax = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    acc += p_of(r);
+    cmax = fmax(cmax, acc);
+  }
+  const double thr = tau * warp_max(cmax);
+  acc = off;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    acc += p_of(r);
+    const int k = lane * R + r;
+    if (k < T_n) flag[2047 - static_cast<int>(v[r] & 0x7FFull)] = (acc <= thr || k == 0) ? 1 : 0;
+  }
+  __syncwarp();
+}
+
+// RS = SORTN / 32 for the register sort (SORTN <= 1024), 0 = the
+// shared-memory sort (SORTN = 2048).
+#ifndef SPARGE_TOPCDF_MINB32
+#define SPARGE_TOPCDF_MINB32 3
+#endif
+template <int RS>
+__global__ void __launch_bounds__(kRowWarps * 32, RS >= 32 ? SPARGE_TOPCDF_MINB32 : 4)
 k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
               const double* __restrict__ k_sim, int Hq, int Hkv, int N, int T_m, int T_n,
               int rows_total, int sortn, int bq, int bk, int causal, double tau, double theta,
@@ -163,9 +260,10 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int row = blockIdx.x * kRowWarps + wid;          // (b*Hq + hq)*T_m + i
   if (row >= rows_total) return;
-  uint64_t* ukey = reinterpret_cast<uint64_t*>(smem) + wid * sortn;
+  const int kstride = sortn + sortn / 32;                 // padded key slots per warp
+  uint64_t* ukey = reinterpret_cast<uint64_t*>(smem) + wid * kstride;
   double* key = reinterpret_cast<double*>(ukey);
-  uint8_t* flag = smem + static_cast<size_t>(kRowWarps) * sortn * 8 + wid * sortn;
+  uint8_t* flag = smem + static_cast<size_t>(kRowWarps) * kstride * 8 + wid * sortn;
 
   const int i = row % T_m, bhq = row / T_m;
   const int hq = bhq % Hq, b = bhq / Hq;
@@ -174,11 +272,14 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   const double* srow = shat + static_cast<int64_t>(row) * T_n;
 
   // ---- S^ row with the -inf columns (fixed K blocks, causally dead) ----
+  // (register-sort rows keep entry j at the padded slot pidx(j) throughout)
+  constexpr bool padded = RS > 0;
+  auto kix = [&](int j) { return padded ? pidx(j) : j; };
   double mx = -INFINITY;
   for (int j = lane; j < T_n; j += 32) {
     const bool dead = causal && (j * bk > last_q);
     const double s = (dead || k_sim[kbase + j] < theta) ? -INFINITY : srow[j];
-    key[j] = s;
+    key[kix(j)] = s;
     mx = fmax(mx, s);
   }
   mx = warp_max(mx);
@@ -187,8 +288,9 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   if (!flagged) {
     double part = 0.0;
     for (int j = lane; j < T_n; j += 32) {
-      const double e = (key[j] == -INFINITY) ? 0.0 : exp(key[j] - mx);
-      key[j] = e;
+      const double kv = key[kix(j)];
+      const double e = (kv == -INFINITY) ? 0.0 : exp(kv - mx);
+      key[kix(j)] = e;
       part += e;
     }
     const double total = warp_sum(part);
@@ -198,6 +300,19 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
     // truncation of P^ -- far inside the 1e-6 near-threshold band of the
     // parity criterion; the cumulative sum uses the truncated values.
     // Padding keys are 0 and sort last (a real entry has key >= 2047 - j > 0).
+    if (RS > 0) {
+      // register sort: composite keys in place at the padded positions,
+      // read back lane-major
+      for (int j = lane; j < sortn; j += 32) {
+        const int pj = pidx(j);
+        ukey[pj] = (j < T_n)
+                       ? ((static_cast<uint64_t>(__double_as_longlong(key[pj] / total)) & ~0x7FFull) |
+                          static_cast<uint64_t>(2047 - j))
+                       : 0ull;
+      }
+      __syncwarp();
+      topcdf_reg<(RS > 0 ? RS : 1)>(ukey, flag, T_n, tau, lane);
+    } else {
     for (int j = lane; j < sortn; j += 32) {
       ukey[j] = (j < T_n)
                     ? ((static_cast<uint64_t>(__double_as_longlong(key[j] / total)) & ~0x7FFull) |
@@ -205,15 +320,7 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
                     : 0ull;
     }
     __syncwarp();
-    switch (sortn) {
-      case 32: sort_desc<32>(ukey, lane); break;
-      case 64: sort_desc<64>(ukey, lane); break;
-      case 128: sort_desc<128>(ukey, lane); break;
-      case 256: sort_desc<256>(ukey, lane); break;
-      case 512: sort_desc<512>(ukey, lane); break;
-      case 1024: sort_desc<1024>(ukey, lane); break;
-      default: sort_desc<2048>(ukey, lane); break;
-    }
+    sort_desc<2048>(ukey, lane);
     // inclusive cumulative sum in rank order, 32 ranks per step (rank
     // 32*s + lane): conflict-free shared-memory reads.  Pass 1 finds c_last,
     // pass 2 recomputes the identical prefix sums and decides.  c_last (R4)
@@ -239,6 +346,7 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
       if (k < T_n) flag[2047 - static_cast<int>(kv & 0x7FFull)] = (c <= thr || k == 0) ? 1 : 0;
     }
     __syncwarp();
+    }
   }
 
   // ---- forcing (Eq. 5), flagged rows, causal live AND + diagonal guard ----
@@ -282,15 +390,26 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
                                                         shat);
   int sortn = 32;
   while (sortn < T_n) sortn <<= 1;
-  const size_t smem_r = static_cast<size_t>(kRowWarps) * sortn * 9;
-  e = cudaFuncSetAttribute(k_topcdf_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem_r));
-  if (e != cudaSuccess) return e;
+  const size_t smem_r = static_cast<size_t>(kRowWarps) * ((sortn + sortn / 32) * 8 + sortn);
   const int rows = s.B * s.Hq * T_m;
-  k_topcdf_rows<<<(rows + kRowWarps - 1) / kRowWarps, kRowWarps * 32, smem_r, stream>>>(
-      shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, sortn, s.bq, s.bk, s.causal,
-      static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
-  return cudaGetLastError();
+  auto run = [&](auto kern) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem_r));
+    if (e2 != cudaSuccess) return e2;
+    kern<<<(rows + kRowWarps - 1) / kRowWarps, kRowWarps * 32, smem_r, stream>>>(
+        shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, sortn, s.bq, s.bk, s.causal,
+        static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
+    return cudaGetLastError();
+  };
+  switch (sortn) {
+    case 32: return run(k_topcdf_rows<1>);
+    case 64: return run(k_topcdf_rows<2>);
+    case 128: return run(k_topcdf_rows<4>);
+    case 256: return run(k_topcdf_rows<8>);
+    case 512: return run(k_topcdf_rows<16>);
+    case 1024: return run(k_topcdf_rows<32>);
+    default: return run(k_topcdf_rows<0>);
+  }
 }
 
 }  // namespace
