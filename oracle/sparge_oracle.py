@@ -28,6 +28,9 @@ __all__ = [
     "top_cdf_rational",
     "predict_mask",
     "causal_live",
+    "E4M3_MAX",
+    "round_e4m3",
+    "fp8_v_quant",
     "round_bf16",
     "sparse_attention",
     "dense_attention",
@@ -288,11 +291,43 @@ def round_bf16(x):
     return np.ldexp(np.rint(m * 256.0) / 256.0, e)
 
 
+E4M3_MAX = 448.0
+
+
+def round_e4m3(x):
+    """Round fp64 values to the nearest FP8 E4M3 value (the OCP "fn" format:
+    3 mantissa bits, bias 7, normals 2^-6 .. 448, subnormals on the 2^-9
+    grid), ties to even, saturating to +-448 -- the P~ and V operands of
+    SageAttention2's FP8 P~V product (footnote P:L44; scope row f4, R27).
+    Directly from fp64 (no double rounding)."""
+    x = np.asarray(x, dtype=np.float64)
+    a = np.abs(x)
+    _, e = np.frexp(a)                   # a = m 2^e, 0.5 <= m < 1 (e = 0 for a = 0)
+    E = np.maximum(e - 1, -6)            # exponent of the leading bit; subnormals share -6
+    q = np.ldexp(1.0, E - 3)             # spacing of representable values around a
+    r = np.minimum(np.rint(a / q) * q, E4M3_MAX)
+    return np.copysign(r, x)
+
+
+def fp8_v_quant(V):
+    """Per-channel FP8 quantisation of V (SageAttention2, R27): over all rows
+    of the head, amax_c = max|V[:, c]| (fp32), inv_c = fl32(448 / amax_c),
+    s_c = fl32(amax_c / 448), V^ = e4m3(fl32(V * inv_c)); an all-zero column
+    has inv_c = s_c = 1.  Returns (V^ fp64 [N, d], s fp32 [d])."""
+    V32 = np.asarray(V, dtype=np.float64).astype(np.float32)
+    amax = np.abs(V32).max(axis=0)
+    nz = amax > 0
+    one = np.float32(1.0)
+    inv = np.where(nz, np.float32(E4M3_MAX) / np.where(nz, amax, one), one).astype(np.float32)
+    sc = np.where(nz, amax / np.float32(E4M3_MAX), one).astype(np.float32)
+    return round_e4m3((V32 * inv[None, :]).astype(np.float64)), sc
+
+
 # --------------------------------------------------------------------------
 # Alg. 1 lines 7-21 (P:L197-223): stage 2, the sparse FlashAttention loop.
 # --------------------------------------------------------------------------
 def sparse_attention(Q, K, V, M, lam, bq=128, bk=64, cw=4, causal=False, quant=None,
-                     pv_round="bf16", qblocks=None):
+                     pv_round="bf16", qblocks=None, v_fp8=None):
     """O for one head, following Algorithm 1 and the online
     softmax of Eq. (1).
 
@@ -302,7 +337,8 @@ def sparse_attention(Q, K, V, M, lam, bq=128, bk=64, cw=4, causal=False, quant=N
             product is exact;
     V: fp64 [N, d];  M: [T_m, T_n] mask (line 10);  lam: lambda (natural-log
     units of S, R3; -inf disables);  pv_round: "bf16" rounds P~ before P~V
-    (R12/R13), None keeps fp64.
+    (R12/R13), None keeps fp64, "fp8" is the f4 product (R27): e4m3(128 P~)
+    times V^ of v_fp8 = fp8_v_quant(V), O = acc * s / (128 l).
     qblocks: optional list of q-block indices to compute (sampling); other
     rows of O are NaN.
 
@@ -358,13 +394,20 @@ def sparse_attention(Q, K, V, M, lam, bq=128, bk=64, cw=4, causal=False, quant=N
                     continue                    # warp with no valid rows (R6)
                 g = np.max(gap[a:b])
                 if g > lam:                     # compute iff > lambda (R5)
-                    Pw = round_bf16(P[a:b]) if pv_round == "bf16" else P[a:b]
-                    Oi[a:b] = alpha[a:b, None] * Oi[a:b] + Pw @ V[c0:c1]
+                    if pv_round == "fp8":
+                        Pw = round_e4m3(P[a:b] * 128.0)
+                        Oi[a:b] = alpha[a:b, None] * Oi[a:b] + Pw @ v_fp8[0][c0:c1]
+                    else:
+                        Pw = round_bf16(P[a:b]) if pv_round == "bf16" else P[a:b]
+                        Oi[a:b] = alpha[a:b, None] * Oi[a:b] + Pw @ V[c0:c1]
                     cnt["pv_slices"] += 1
             m = m_new
         if np.any(l == 0):
             raise OracleInvariantError(f"q-block {i}: a row finished with l = 0")
-        O[r0:r1] = Oi / l[:, None]              # line 19: O_i = diag(l)^-1 O_i
+        if pv_round == "fp8":                   # dequantise: per-channel s, the 128 of P~
+            O[r0:r1] = Oi * v_fp8[1].astype(np.float64)[None, :] / (128.0 * l[:, None])
+        else:
+            O[r0:r1] = Oi / l[:, None]          # line 19: O_i = diag(l)^-1 O_i
     return O, cnt
 
 
@@ -415,5 +458,7 @@ def spargeattn_head(q, k, v, tau, theta, lam, bq=128, bk=64, cw=4, causal=False,
         Qq, dq = quantize_blocks(q, bq)
         Kq, dk = quantize_blocks(k, bk)
         quant = (Qq, dq, Kq, dk)
-    O, cnt = sparse_attention(q, k, v, M, lam, bq, bk, cw, causal, quant, pv_round, qblocks)
+    v_fp8 = fp8_v_quant(v) if pv_round == "fp8" else None
+    O, cnt = sparse_attention(q, k, v, M, lam, bq, bk, cw, causal, quant, pv_round, qblocks,
+                              v_fp8)
     return O, M, near, cnt, quant
