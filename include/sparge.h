@@ -44,6 +44,13 @@ enum sparge_status {
 };
 
 enum sparge_dtype { SPARGE_BF16 = 0, SPARGE_FP16 = 1 };
+/* Operand type of the P~V product (Alg. 1 line 16):
+ *   SPARGE_PV_SAME_AS_INPUT  P~ rounded to in_dtype, V in in_dtype (R12);
+ *   SPARGE_PV_FP8_E4M3       scope row f4 (SageAttention2-style, footnote
+ *                            P:L44; R27): V per-channel FP8 E4M3 with
+ *                            s_c = amax_c / 448 over all N tokens of its kv-head,
+ *                            P~ scaled by 2^7 and rounded to E4M3, fp32
+ *                            accumulation, O = acc * s_c / l.  INT8 QK only. */
 enum sparge_pv_dtype { SPARGE_PV_SAME_AS_INPUT = 0, SPARGE_PV_FP8_E4M3 = 1 };
 /* Operand type of the QK^T product (stage 2, Alg. 1 line 12):
  *   SPARGE_QK_INT8   SageAttention per-block INT8 -- the
@@ -64,7 +71,7 @@ typedef struct {
   int bq, bk, cw;         /* must be 128, 64, 4                            */
   int causal;             /* 0/1; block-causal handling per reading R8      */
   int in_dtype;           /* enum sparge_dtype of Q, K, V, O                 */
-  int pv_dtype;           /* enum sparge_pv_dtype (FP8 -> SPARGE_ENOTIMPL)   */
+  int pv_dtype;           /* enum sparge_pv_dtype                            */
   int sim_mode;           /* enum sparge_sim_mode                           */
   int smooth_k;           /* 0 only (R14); 1 -> SPARGE_ENOTIMPL              */
   int qk_dtype;           /* enum sparge_qk_dtype                           */
@@ -150,8 +157,10 @@ int sparge_predict_mask(const sparge_shape* shape,
  * map S^, B*Hq*T_m*T_n doubles).  0 on invalid shape. */
 size_t sparge_predict_workspace(const sparge_shape* shape);
 
-/* Bytes of device workspace sparge_attn_fwd needs for `shape` (V^T staging,
- * work list, status word).  0 on invalid shape. */
+/* Bytes of device workspace sparge_attn_fwd needs for `shape`: the status
+ * word (256 B), the V^T staging (16-bit, or E4M3 for pv_dtype FP8, rounded
+ * to 256 B) and, for FP8, the per-channel amax and dequant scales.  0 on
+ * invalid shape. */
 size_t sparge_attn_workspace(const sparge_shape* shape);
 
 /*
@@ -180,7 +189,8 @@ size_t sparge_attn_workspace(const sparge_shape* shape);
  *   workspace/ws_bytes  >= sparge_attn_workspace(shape), 256-byte aligned;
  *            zero-initialised once by the caller (its first word is the
  *            status word, cleared again by sparge_attn_status)
- * Errors: SPARGE_EINVAL, SPARGE_ENOTIMPL (pv_dtype FP8), SPARGE_ECUDA.  A
+ * Errors: SPARGE_EINVAL, SPARGE_ENOTIMPL (pv_dtype FP8 with qk_dtype INPUT,
+ * smooth_k), SPARGE_ECUDA.  A
  * row finishing with l = 0 is recorded in the workspace status word and
  * reported by sparge_attn_status.
  */

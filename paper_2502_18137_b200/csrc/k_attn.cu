@@ -99,14 +99,14 @@ struct Roles {
 // kernel (16-bit Q, K tiles stored as d/64 SWIZZLE_128B K-atoms of 128 B
 // rows); with d = 128 its rings shrink to 2 + 2 stages so that two groups
 // still fit on an SM.
-template <int D, bool QK16>
+template <int D, bool QK16, bool PV8 = false>
 struct Smem {
   static constexpr int EB = QK16 ? 2 : 1;       // bytes per Q/K element
   static constexpr int KST = (QK16 && D == 128) ? 2 : 4;   // K stages
-  static constexpr int VST = (QK16 && D == 128) ? 2 : 3;   // V^T stages
+  static constexpr int VST = (QK16 && D == 128) ? 2 : (PV8 ? 4 : 3);   // V^T stages
   static constexpr int Q_BYTES = BQ * D * EB;
   static constexpr int K_BYTES = BK * D * EB;
-  static constexpr int V_BYTES = D * BK * 2;    // V^T tile, 16-bit
+  static constexpr int V_BYTES = D * BK * (PV8 ? 1 : 2);    // V^T tile, 16-bit or e4m3
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * K_BYTES;
@@ -132,6 +132,7 @@ struct AttnParams {
   int64_t o_sb, o_sh, o_sn;
   unsigned long long* counters;
   unsigned int* status;
+  const float* v_scale;   // PV8: per-(b, hkv, channel) dequant scale s_c [B*Hkv, D]
   float lam2;         // lambda * log2(e)
   float scale_log2;   // log2(e) / sqrt(d)
   int N, T_m, T_n, Hq, Hkv, group;
@@ -187,6 +188,22 @@ template <bool F16>
 __device__ __forceinline__ uint32_t pack16(float lo, float hi) {
   return F16 ? pack_f16x2(lo, hi) : pack_bf16x2(lo, hi);
 }
+// two fp32 -> FP8 E4M3 (round to nearest even, saturate to +-448), lo in the
+// low byte
+__device__ __forceinline__ uint32_t pack_e4m3x2(float lo, float hi) {
+  unsigned short r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void mma_f8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 // P~ = exp2(acc * c - m_ref) for the 64 columns of a row, packed to 16-bit,
 // and their sum.  bits(acc + 0x4B400000) are the fp32 value M + acc,
@@ -197,7 +214,8 @@ __device__ __forceinline__ uint32_t pack16(float lo, float hi) {
 // integer accumulator, far below the INT8 quantisation error in acc (R23).
 // MASKED: INT_MIN entries and rows without a finite reference give 0.
 // QK16: a holds fp32 S accumulators (no magic constant); masked entries -inf.
-template <bool MASKED, bool F16, bool QK16 = false>
+// PV8: P~ packed to FP8 E4M3, four per word (pw[16]).
+template <bool MASKED, bool F16, bool QK16 = false, bool PV8 = false>
 __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, uint32_t* pw,
                                        float& sum) {
   constexpr int kAdd = QK16 ? 0 : kMagic;
@@ -222,17 +240,26 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
       e2 = pk(e0, e1);
     }
     rs2[(k >> 1) & 1] = add2(rs2[(k >> 1) & 1], e2);
-    pw[k >> 1] = pack16<F16>(lo_f(e2), hi_f(e2));
+    if (PV8) {
+      const uint32_t h = pack_e4m3x2(lo_f(e2), hi_f(e2));
+      if ((k & 2) == 0) pw[k >> 2] = h;
+      else pw[k >> 2] |= h << 16;
+    } else {
+      pw[k >> 1] = pack16<F16>(lo_f(e2), hi_f(e2));
+    }
   }
   const uint64_t rs = add2(rs2[0], rs2[1]);
   sum = lo_f(rs) + hi_f(rs);
 }
 
-template <int D, bool CAUSAL, bool F16, bool QK16, int NG>
+template <int D, bool CAUSAL, bool F16, bool QK16, int NG, bool PV8>
 __global__ void __launch_bounds__(Roles<NG>::THREADS, 2 / NG)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  using L = Smem<D, QK16>;
+  using L = Smem<D, QK16, PV8>;
+  // FP8 P~ (f4) is rounded relative to the reference max: rescale eagerly so
+  // the reference is the true running max (R27), as the oracle's P~ = e^{S-m}
+  constexpr float kRefThreshold = PV8 ? 0.0f : kRescaleThreshold;
   using R = Roles<NG>;
   constexpr int KST = L::KST, VST = L::VST;
   extern __shared__ unsigned char smem_raw[];
@@ -344,7 +371,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     if (lane == 0 && n_tiles > 0) {
       constexpr uint32_t IDESC_QK =
           QK16 ? (F16 ? idesc_f16(BQ, BK) : idesc_bf16(BQ, BK)) : idesc_i8(BQ, BK);
-      constexpr uint32_t IDESC_PV = F16 ? idesc_f16(BQ, D) : idesc_bf16(BQ, D);
+      // (kind::f8f6f4 with E4M3 A/B and fp32 D has the f16 field values)
+      constexpr uint32_t IDESC_PV = (F16 || PV8) ? idesc_f16(BQ, D) : idesc_bf16(BQ, D);
       const uint64_t dQ = umma_desc_kmajor(smem_u32(sQ), L::ROW_BYTES_QK);
       unsigned long long issued = 0;
       mbar_wait(q_full, 0);
@@ -357,11 +385,19 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         const bool any = (pv_flag[pb * 4 + 0] | pv_flag[pb * 4 + 1] |
                           pv_flag[pb * 4 + 2] | pv_flag[pb * 4 + 3]) != 0;
         if (any) {
-          const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
-          const uint32_t tP = tS0 + pb * BK;     // P~ 16-bit, 32 packed columns
+          const uint32_t tP = tS0 + pb * BK;     // P~ 16-bit (32 cols) or e4m3 (16 cols)
+          if (PV8) {
+            // K = 32 e4m3 per kind::f8f6f4 MMA: 8 TMEM cols of P~, 32 B of V^T rows
+            const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 64);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
-            mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
+            for (int kk = 0; kk < BK / 32; ++kk)
+              mma_f8_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
+          } else {
+            const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
+              mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
+          }
           ++issued;
         }
         tc_commit(v_empty + vs);
@@ -514,7 +550,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         compute = __any_sync(0xffffffffu, row_has && (m_loc - m_new > p.lam2));
         // lazy rescale (R22): move the reference max only when it lags the
         // true max by more than the threshold (always when it is -inf)
-        need = compute && (m_new > m_ref + kRescaleThreshold);
+        need = compute && (m_new > m_ref + kRefThreshold);
         rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
         if (need) {
           alpha = ex2_approx(m_ref - m_new);   // 0 when m_ref = -inf (l, O are 0 then)
@@ -530,8 +566,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       uint32_t pw[BK / 2];
       {
         float rsum;
-        if (need_mask) exps64<true, F16, QK16>(a, c, m_ref, pw, rsum);
-        else exps64<false, F16, QK16>(a, c, m_ref, pw, rsum);
+        // PV8: P~' = 2^7 P~ (E4M3 range and precision; l carries the same
+        // factor, so O = acc * s_c / l needs no extra scale)
+        const float mr = PV8 ? m_ref - 7.0f : m_ref;
+        if (need_mask) exps64<true, F16, QK16, PV8>(a, c, mr, pw, rsum);
+        else exps64<false, F16, QK16, PV8>(a, c, mr, pw, rsum);
         l += rsum;           // R9: skipped groups still add their mass to l
       }
       if (PP && !(g == 1 && t == n_iter - 1)) named_bar_arrive(other_bar, 64);
@@ -539,7 +578,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       {
         if (!compute) {
 #pragma unroll
-          for (int k = 0; k < BK / 2; ++k) pw[k] = 0u;
+          for (int k = 0; k < (PV8 ? BK / 4 : BK / 2); ++k) pw[k] = 0u;
         }
         PT_MARK(4);
 
@@ -563,7 +602,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         // P~(t) overwrites the first 32 columns of S[sb]: S(t) is already in
         // registers, and QK(t) -- complete, per s_full -- executed after
         // P~V(t-2), the previous reader of this buffer.
-        tmem_st32(tS, pw);
+        if (PV8) tmem_st16(tS, pw);
+        else tmem_st32(tS, pw);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -594,12 +634,18 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     if (row_valid && !(l > 0.f)) atomicOr(p.status, 1u);
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
     const int dst_row = row_valid ? (p.perm ? __ldg(p.perm + row_g) : row_g) : 0;
+    const float* vsc = PV8 ? p.v_scale + static_cast<int64_t>(bkv) * D : nullptr;
     uint16_t* orow = p.o + b * p.o_sb + hq * p.o_sh + static_cast<int64_t>(dst_row) * p.o_sn;
 #pragma unroll
     for (int cc = 0; cc < D / 32; ++cc) {
       uint32_t ov[32];
       tmem_ld32(tO + lane_base + cc * 32, ov);
       tmem_wait_ld();
+      if (PV8) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          ov[k] = __float_as_uint(__uint_as_float(ov[k]) * __ldg(vsc + cc * 32 + k));
+      }
       if (row_valid) {
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
@@ -628,12 +674,12 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   }
 }
 
-template <int D, bool CAUSAL, bool F16, bool QK16>
+template <int D, bool CAUSAL, bool F16, bool QK16, bool PV8 = false>
 cudaError_t launch_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                      const AttnParams& p, int B, cudaStream_t stream) {
   constexpr int NG = kPairs ? 2 : 1;
-  auto kern = k_sparse_attn<D, CAUSAL, F16, QK16, NG>;
-  const int smem = NG * Smem<D, QK16>::GROUP + 1024;   // + slack for 1024-B alignment
+  auto kern = k_sparse_attn<D, CAUSAL, F16, QK16, NG, PV8>;
+  const int smem = NG * Smem<D, QK16, PV8>::GROUP + 1024;   // + slack for 1024-B alignment
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   dim3 grid((p.T_m + NG - 1) / NG, B * p.Hq);
@@ -647,8 +693,10 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
                         const CUtensorMap& mv, const float* dq, const float* dk,
                         const int32_t* lut, const int32_t* cnt, float lambda,
                         const int32_t* perm, void* o, sparge_strides o_str,
-                        uint64_t* counters, unsigned int* status, cudaStream_t stream) {
+                        uint64_t* counters, unsigned int* status, const float* v_scale,
+                        cudaStream_t stream) {
   AttnParams p;
+  p.v_scale = v_scale;
   p.dq = dq; p.dk = dk; p.lut = lut; p.cnt = cnt; p.perm = perm;
   p.o = static_cast<uint16_t*>(o);
   p.o_sb = o_str.b; p.o_sh = o_str.h; p.o_sn = o_str.n;
@@ -663,9 +711,11 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
   p.phase_clk = reinterpret_cast<unsigned long long*>(status + 8);   // debug builds only
   const bool f16 = s.in_dtype == SPARGE_FP16;
   const bool qk16 = s.qk_dtype == SPARGE_QK_INPUT;
+  const bool pv8 = s.pv_dtype == SPARGE_PV_FP8_E4M3;   // INT8 QK only (validated)
 #define SPARGE_A(D, C, F)                                                      \
   return qk16 ? launch_t<D, C, F, true>(mq, mk, mv, p, s.B, stream)            \
-              : launch_t<D, C, F, false>(mq, mk, mv, p, s.B, stream)
+              : (pv8 ? launch_t<D, C, F, false, true>(mq, mk, mv, p, s.B, stream) \
+                     : launch_t<D, C, F, false>(mq, mk, mv, p, s.B, stream))
   if (s.d == 128) {
     if (s.causal) { if (f16) SPARGE_A(128, true, true); else SPARGE_A(128, true, false); }
     else          { if (f16) SPARGE_A(128, false, true); else SPARGE_A(128, false, false); }

@@ -41,6 +41,18 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 int n_pad_of(const sparge_shape* s) { return ((s->N + 63) / 64) * 64; }
 
+// Workspace: [status 256 B][V^T: 16-bit, or e4m3 for pv_dtype FP8]
+// (FP8 adds [amax bits u32 B*Hkv*d][dequant scales f32 B*Hkv*d], 256-aligned)
+size_t round256(size_t x) { return (x + 255) / 256 * 256; }
+size_t vt_bytes(const sparge_shape* s) {
+  const size_t eb = s->pv_dtype == SPARGE_PV_FP8_E4M3 ? 1 : 2;
+  return round256(static_cast<size_t>(s->B) * s->Hkv * s->d * n_pad_of(s) * eb);
+}
+size_t chan_bytes(const sparge_shape* s) {
+  return round256(static_cast<size_t>(s->B) * s->Hkv * s->d * 4);
+}
+
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -136,8 +148,8 @@ int sparge_predict_mask(const sparge_shape* shape, const double* q_pooled, const
 
 size_t sparge_attn_workspace(const sparge_shape* shape) {
   if (!shape_ok(shape)) return 0;
-  const size_t vt = static_cast<size_t>(shape->B) * shape->Hkv * shape->d * n_pad_of(shape) * 2;
-  return kStatusBytes + vt;
+  const size_t extra = shape->pv_dtype == SPARGE_PV_FP8_E4M3 ? 2 * chan_bytes(shape) : 0;
+  return kStatusBytes + vt_bytes(shape) + extra;
 }
 
 int sparge_attn_fwd(const sparge_shape* shape, const void* qq, const float* dq,
@@ -163,7 +175,8 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
   if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return SPARGE_EINVAL;
   if (ws_bytes < sparge_attn_workspace(shape)) return SPARGE_EINVAL;
   if (!(lambda < 0.f)) return SPARGE_EINVAL;   // lambda < 0 or -inf (§3.6)
-  if (shape->pv_dtype != SPARGE_PV_SAME_AS_INPUT) return SPARGE_ENOTIMPL;
+  const bool pv8 = shape->pv_dtype == SPARGE_PV_FP8_E4M3;
+  if (pv8 && shape->qk_dtype != SPARGE_QK_INT8) return SPARGE_ENOTIMPL;   // FP8 PV with INT8 QK only
   if (shape->smooth_k) return SPARGE_ENOTIMPL;
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -172,10 +185,14 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   unsigned int* status = reinterpret_cast<unsigned int*>(ws);
   void* vt = ws + kStatusBytes;
+  unsigned int* amax_bits = reinterpret_cast<unsigned int*>(ws + kStatusBytes + vt_bytes(shape));
+  float* v_scale = reinterpret_cast<float*>(ws + kStatusBytes + vt_bytes(shape) + chan_bytes(shape));
 
   cudaError_t e = cudaSuccess;
   if (!(flags & SPARGE_ATTN_SKIP_VPREP)) {
-    e = launch_vprep(s, v, v_str, perm, vt, n_pad, st);
+    e = pv8 ? launch_vprep_fp8(s, v, v_str, perm, static_cast<uint8_t*>(vt), amax_bits, v_scale,
+                               n_pad, st)
+            : launch_vprep(s, v, v_str, perm, vt, n_pad, st);
     if (e != cudaSuccess) return SPARGE_ECUDA;
   }
   if (flags & SPARGE_ATTN_VPREP_ONLY) return SPARGE_OK;
@@ -198,12 +215,16 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
                 box0, 128, sw_qk) ||
       !encode3d(&mk, dt_qk, kq, d, N, static_cast<uint64_t>(s.B) * s.Hkv, d * eb, d * N * eb,
                 box0, 64, sw_qk) ||
-      !encode3d(&mv, dt16, vt, static_cast<uint64_t>(n_pad), d, static_cast<uint64_t>(s.B) * s.Hkv,
-                static_cast<uint64_t>(n_pad) * 2, d * n_pad * 2, 64, s.d,
-                CU_TENSOR_MAP_SWIZZLE_128B))
+      !(pv8 ? encode3d(&mv, CU_TENSOR_MAP_DATA_TYPE_UINT8, vt, static_cast<uint64_t>(n_pad), d,
+                       static_cast<uint64_t>(s.B) * s.Hkv, static_cast<uint64_t>(n_pad), d * n_pad,
+                       64, s.d, CU_TENSOR_MAP_SWIZZLE_64B)
+            : encode3d(&mv, dt16, vt, static_cast<uint64_t>(n_pad), d,
+                       static_cast<uint64_t>(s.B) * s.Hkv, static_cast<uint64_t>(n_pad) * 2,
+                       d * n_pad * 2, 64, s.d, CU_TENSOR_MAP_SWIZZLE_128B)))
     return SPARGE_ECUDA;
 
-  e = launch_attn(s, mq, mk, mv, dq, dk, lut, cnt, lambda, perm, o, o_str, counters, status, st);
+  e = launch_attn(s, mq, mk, mv, dq, dk, lut, cnt, lambda, perm, o, o_str, counters, status,
+                  pv8 ? v_scale : nullptr, st);
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
 }
 

@@ -21,12 +21,18 @@ size_t predict_workspace_bytes(const sparge_shape& s);
 
 cudaError_t launch_vprep(const sparge_shape& s, const void* v, sparge_strides st,
                          const int32_t* perm, void* vt, int n_pad, cudaStream_t stream);
+// f4: per-channel amax of V (into amax_bits, zeroed here), then V^T in FP8
+// E4M3 (x * fl32(448/amax_c)) and the dequant scales s_c = fl32(amax_c/448).
+cudaError_t launch_vprep_fp8(const sparge_shape& s, const void* v, sparge_strides st,
+                             const int32_t* perm, uint8_t* vt8, unsigned int* amax_bits,
+                             float* v_scale, int n_pad, cudaStream_t stream);
 
 cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUtensorMap& mk,
                         const CUtensorMap& mv, const float* dq, const float* dk,
                         const int32_t* lut, const int32_t* cnt, float lambda,
                         const int32_t* perm, void* o, sparge_strides o_str,
-                        uint64_t* counters, unsigned int* status, cudaStream_t stream);
+                        uint64_t* counters, unsigned int* status, const float* v_scale,
+                        cudaStream_t stream);
 
 int attn_smem_bytes(int d, int qk16);
 

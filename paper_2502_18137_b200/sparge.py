@@ -21,6 +21,8 @@ SPARGE_BF16, SPARGE_FP16 = 0, 1
 SPARGE_SIM_COSINE, SPARGE_SIM_LITERAL = 0, 1
 # QK^T operand: INT8 (SageAttention, the default) or the input dtype ("SpargeAttn+FA2", row f1)
 SPARGE_QK_INT8, SPARGE_QK_INPUT = 0, 1
+# P~V operand: the input dtype (default) or FP8 E4M3 (SageAttention2-style, row f4)
+SPARGE_PV_SAME_AS_INPUT, SPARGE_PV_FP8_E4M3 = 0, 1
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2502_18137_b200.build` "
@@ -102,9 +104,9 @@ def _strides(t):
 
 
 def make_shape(B, Hq, Hkv, N, d, causal=False, dtype=torch.bfloat16, sim_mode=SPARGE_SIM_COSINE,
-               qk_dtype=SPARGE_QK_INT8):
+               qk_dtype=SPARGE_QK_INT8, pv_dtype=SPARGE_PV_SAME_AS_INPUT):
     return Shape(B, Hq, Hkv, N, d, 128, 64, 4, int(bool(causal)),
-                 SPARGE_FP16 if dtype == torch.float16 else SPARGE_BF16, 0, sim_mode, 0,
+                 SPARGE_FP16 if dtype == torch.float16 else SPARGE_BF16, int(pv_dtype), sim_mode, 0,
                  int(qk_dtype))
 
 
@@ -219,15 +221,17 @@ class Buffers:
 
 
 def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=None, out=None,
-                   sim_mode=SPARGE_SIM_COSINE, stream=None, qk_dtype=SPARGE_QK_INT8):
+                   sim_mode=SPARGE_SIM_COSINE, stream=None, qk_dtype=SPARGE_QK_INT8,
+                   pv_dtype=SPARGE_PV_SAME_AS_INPUT):
     """The whole hot path (a1 quantise Q, K -> a2 predict -> a3 attention) on
     device tensors q [B,Hq,N,d], k/v [B,Hkv,N,d] (bf16 or fp16).  perm: optional
     int32 device tensor [N] (Hilbert order); O is returned in original order.
-    qk_dtype=SPARGE_QK_INPUT selects the unquantised "SpargeAttn+FA2" kernel.
+    qk_dtype=SPARGE_QK_INPUT selects the unquantised "SpargeAttn+FA2" kernel;
+    pv_dtype=SPARGE_PV_FP8_E4M3 the FP8 P~V product (row f4).
     Returns (O, buffers)."""
     B, Hq, N, d = q.shape
     Hkv = k.shape[1]
-    shape = make_shape(B, Hq, Hkv, N, d, causal, q.dtype, sim_mode, qk_dtype)
+    shape = make_shape(B, Hq, Hkv, N, d, causal, q.dtype, sim_mode, qk_dtype, pv_dtype)
     if buffers is None:
         buffers = Buffers(shape, device=q.device)
     bf = buffers
