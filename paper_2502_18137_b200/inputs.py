@@ -159,6 +159,9 @@ WORKLOADS = {
                          Hkv=30, causal=False, hilbert=True),
     "mochi": dict(kind="video", T=28, H=30, W=53, text_prefix=0, d=128, Hq=24, Hkv=24,
                   causal=False, hilbert=True),
+    # the paper's own Mochi run is ~22K tokens: half the latent frames
+    "mochi_22k": dict(kind="video", T=14, H=30, W=53, text_prefix=0, d=128, Hq=24, Hkv=24,
+                      causal=False, hilbert=True),
     "sweep_8k": dict(kind="llm_local", N=8192, d=128, Hq=32, Hkv=32, causal=False),
     "sweep_16k": dict(kind="llm_local", N=16384, d=128, Hq=32, Hkv=32, causal=False),
     "sweep_32k": dict(kind="llm_local", N=32768, d=128, Hq=32, Hkv=32, causal=False),
