@@ -48,6 +48,25 @@
 #include "sm100.cuh"
 #include "sparge_internal.h"
 
+// SPARGE_CTA_TIMING (debug builds only): per-CTA globaltimer records
+// {entry, softmax loop start, loop end, exit, smid, n_tiles} in a device
+// array read back by sparge_debug_cta_records (scripts/cta_timeline.py).
+#ifdef SPARGE_CTA_TIMING
+__device__ unsigned long long g_cta_rec[1 << 16][6];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_REC(slot, val)                                                               \
+  do {                                                                                   \
+    const unsigned cid = blockIdx.y * gridDim.x + blockIdx.x;                           \
+    if (cid < (1u << 16)) g_cta_rec[cid][slot] = (val);                                  \
+  } while (0)
+#else
+#define CTA_REC(slot, val) do { } while (0)
+#endif
+
 #ifdef SPARGE_PHASE_TIMING
 #define PT_MARK(k) do { const long long _c = clock64(); ph[k] += _c - ph_last; ph_last = _c; } while (0)
 #else
@@ -257,6 +276,14 @@ __global__ void __launch_bounds__(Roles<NG>::THREADS, 2 / NG)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
   using L = Smem<D, QK16, PV8>;
+#ifdef SPARGE_CTA_TIMING
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    CTA_REC(0, gtimer());
+    CTA_REC(4, smid);
+  }
+#endif
   // FP8 P~ (f4) is rounded relative to the reference max: rescale eagerly so
   // the reference is the true running max (R27), as the oracle's P~ = e^{S-m}
   constexpr float kRefThreshold = PV8 ? 0.0f : kRescaleThreshold;
@@ -476,6 +503,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
     long long ph_last = clock64();
 #endif
+#ifdef SPARGE_CTA_TIMING
+    if (threadIdx.x == 0) { CTA_REC(1, gtimer()); CTA_REC(5, n_tiles); }
+#endif
     for (int t = 0; t < n_tiles; ++t) {
       const int sb = t & 1;
       const uint32_t tS = tS0 + sb * BK + lane_base;
@@ -628,6 +658,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       atomicAdd(p.phase_clk + 7, static_cast<unsigned long long>(n_tiles));
 #endif
 
+#ifdef SPARGE_CTA_TIMING
+    if (threadIdx.x == 0) CTA_REC(2, gtimer());
+#endif
     // ---- epilogue: O_i = O / l (line 19), scattered back through perm ----
     if (n_tiles > 0) mbar_wait(o_done + ((n_tiles - 1) & 1), ((n_tiles - 1) >> 1) & 1);
     tc_fence_after();
@@ -672,6 +705,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     tc_fence_after();
     tmem_dealloc<256 * NG>(tmem_base);
   }
+#ifdef SPARGE_CTA_TIMING
+  if (threadIdx.x == 0) CTA_REC(3, gtimer());
+#endif
 }
 
 template <int D, bool CAUSAL, bool F16, bool QK16, bool PV8 = false>
@@ -725,6 +761,14 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
   }
 #undef SPARGE_A
 }
+
+#ifdef SPARGE_CTA_TIMING
+}  // namespace sparge
+extern "C" int sparge_debug_cta_records(void* host_dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(host_dst, g_cta_rec, bytes) == cudaSuccess ? 0 : 4;
+}
+namespace sparge {
+#endif
 
 int attn_smem_bytes(int d, int qk16) {
   const int ng = kPairs ? 2 : 1;
