@@ -80,7 +80,13 @@ namespace {
 constexpr int BQ = 128;
 constexpr int BK = 64;
 constexpr int NSOFT = 4;      // softmax warps per query tile: one per TMEM lane quadrant
-constexpr float kRescaleThreshold = 8.0f;   // log2 units
+#ifndef SPARGE_RESCALE_THR
+#define SPARGE_RESCALE_THR 8
+#endif
+// lazy-rescale threshold (R22), log2 units: P~ <= 2^thr, which fp16 P~ must
+// hold (max 65504 < 2^16)
+constexpr float kRescaleThreshold = static_cast<float>(SPARGE_RESCALE_THR);
+constexpr float kRescaleThresholdF16 = SPARGE_RESCALE_THR < 15 ? SPARGE_RESCALE_THR : 15.0f;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kMagic = 0x4B400000;          // bits of 1.5 * 2^23
 constexpr float kMagicF = 12582912.0f;
@@ -106,6 +112,14 @@ constexpr bool kPairs = SPARGE_PAIR != 0;
 #endif
 constexpr bool kPingPong = SPARGE_PINGPONG != 0;
 
+// SPARGE_SPEC (experiment, off: measured slower on Llama/Mochi/CogVideoX):
+// interior tiles compute P~ with the current
+// reference max before the row max is known (see the softmax loop).
+#ifndef SPARGE_SPEC
+#define SPARGE_SPEC 0
+#endif
+constexpr bool kSpec = SPARGE_SPEC != 0 && !kPairs;
+
 template <int NG>
 struct Roles {
   static constexpr int SOFT = NSOFT * NG;        // softmax warps 4g .. 4g+3
@@ -118,6 +132,19 @@ struct Roles {
 // kernel (16-bit Q, K tiles stored as d/64 SWIZZLE_128B K-atoms of 128 B
 // rows); with d = 128 its rings shrink to 2 + 2 stages so that two groups
 // still fit on an SM.
+// SPARGE_BIAS_MMA (INT8 QK): before the kind::i8 MMAs of a tile, one
+// kind::f16 MMA (M128 N64 K16, constant operands 1.0 x 1.5*2^19 summed over
+// K = 16) writes the fp32 value 1.5*2^23 into every S accumulator; the i8
+// MMAs then accumulate onto those bits as int32, so S leaves the tensor core
+// as bits(1.5*2^23 + acc) -- the exact fp32 value 1.5*2^23 + acc (R23)
+// without a per-element integer add in the softmax warps.
+#ifndef SPARGE_BIAS_MMA
+#define SPARGE_BIAS_MMA 1
+#endif
+constexpr bool kBiasMma = SPARGE_BIAS_MMA != 0;
+constexpr uint16_t kBf16One = 0x3F80;        // bf16 1.0
+constexpr uint16_t kBf16MagicPart = 0x4940;  // bf16 786432 = 1.5*2^19 (x 16 = 1.5*2^23)
+
 template <int D, bool QK16, bool PV8 = false>
 struct Smem {
   static constexpr int EB = QK16 ? 2 : 1;       // bytes per Q/K element
@@ -126,10 +153,16 @@ struct Smem {
   static constexpr int Q_BYTES = BQ * D * EB;
   static constexpr int K_BYTES = BK * D * EB;
   static constexpr int V_BYTES = D * BK * (PV8 ? 1 : 2);    // V^T tile, 16-bit or e4m3
+  static constexpr bool BIAS = kBiasMma && !QK16;
+  // constant bias-MMA operands: A 128 x 16 bf16 ones, B 64 x 16 bf16 1.5*2^19
+  static constexpr int CA_BYTES = BIAS ? BQ * 16 * 2 : 0;
+  static constexpr int CB_BYTES = BIAS ? BK * 16 * 2 : 0;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * K_BYTES;
-  static constexpr int OFF_BAR = OFF_V + VST * V_BYTES;
+  static constexpr int OFF_CA = OFF_V + VST * V_BYTES;
+  static constexpr int OFF_CB = OFF_CA + CA_BYTES;
+  static constexpr int OFF_BAR = OFF_CB + CB_BYTES;
   static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 3;
   static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;    // [0] TMEM base, [1..8] pv flags
   static constexpr int TOTAL = OFF_MISC + 64;
@@ -234,11 +267,20 @@ __device__ __forceinline__ void mma_f8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
 // MASKED: INT_MIN entries and rows without a finite reference give 0.
 // QK16: a holds fp32 S accumulators (no magic constant); masked entries -inf.
 // PV8: P~ packed to FP8 E4M3, four per word (pw[16]).
-template <bool MASKED, bool F16, bool QK16 = false, bool PV8 = false>
+// S encodings (SBits): the int32 accumulator (kAdd = magic, masked INT_MIN),
+// the bias-MMA fp32 bits of 1.5*2^23 + acc (kAdd = 0, masked 0), or fp32 S
+// of the unquantised kernel (kAdd = 0, masked -inf).
+template <bool QK16, bool BIAS>
+struct SBits {
+  static constexpr int kAdd = (QK16 || BIAS) ? 0 : kMagic;
+  static constexpr int kMasked = QK16 ? static_cast<int>(0xFF800000u) : (BIAS ? 0 : INT_MIN);
+};
+
+template <bool MASKED, bool F16, bool QK16 = false, bool PV8 = false, bool BIAS = false>
 __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, uint32_t* pw,
                                        float& sum) {
-  constexpr int kAdd = QK16 ? 0 : kMagic;
-  constexpr int kMaskedBits = QK16 ? static_cast<int>(0xFF800000u) : INT_MIN;
+  constexpr int kAdd = SBits<QK16, BIAS>::kAdd;
+  constexpr int kMaskedBits = SBits<QK16, BIAS>::kMasked;
   const uint64_t c2 = pk(c, c);
   const float nbias = QK16 ? -m_ref : fmaf(-kMagicF, c, -m_ref);
   const uint64_t nb2 = pk(nbias, nbias);
@@ -252,7 +294,11 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
     if (!MASKED && kPolyEvery > 0 && ((k >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
       e2 = exp2_poly2(x2);
     else
+#ifdef SPARGE_ABL_NOEXP   // timing ablation only (wrong results): no MUFU
+      e2 = fma2(x2, pk(1e-3f, 1e-3f), pk(1.f, 1.f));
+#else
       e2 = pk(ex2_approx(lo_f(x2)), ex2_approx(hi_f(x2)));
+#endif
     if (MASKED) {
       const float e0 = (a[k] == kMaskedBits || !row_live) ? 0.f : lo_f(e2);
       const float e1 = (a[k + 1] == kMaskedBits || !row_live) ? 0.f : hi_f(e2);
@@ -286,7 +332,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 #endif
   // FP8 P~ (f4) is rounded relative to the reference max: rescale eagerly so
   // the reference is the true running max (R27), as the oracle's P~ = e^{S-m}
-  constexpr float kRefThreshold = PV8 ? 0.0f : kRescaleThreshold;
+  constexpr float kRefThreshold = PV8 ? 0.0f : (F16 ? kRescaleThresholdF16 : kRescaleThreshold);
   using R = Roles<NG>;
   constexpr int KST = L::KST, VST = L::VST;
   extern __shared__ unsigned char smem_raw[];
@@ -325,6 +371,19 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       }
     }
     fence_mbar_init();
+  }
+  if constexpr (L::BIAS) {
+    // constant operands of the bias MMA (every element equal, so the core
+    // matrix layout of the descriptor is immaterial)
+    constexpr uint32_t kOnes = kBf16One | (static_cast<uint32_t>(kBf16One) << 16);
+    constexpr uint32_t kParts = kBf16MagicPart | (static_cast<uint32_t>(kBf16MagicPart) << 16);
+#pragma unroll
+    for (int gg = 0; gg < NG; ++gg) {
+      uint32_t* cw = reinterpret_cast<uint32_t*>(smem0 + gg * L::GROUP + L::OFF_CA);
+      for (int x = threadIdx.x; x < (L::CA_BYTES + L::CB_BYTES) / 4; x += blockDim.x)
+        cw[x] = x < L::CA_BYTES / 4 ? kOnes : kParts;
+    }
+    fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
   }
   if (warp == R::MMA0) tmem_alloc<256 * NG>(tmem_base_slot);
   tc_fence_before();
@@ -379,6 +438,14 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         if (t + 1 < n_tiles) j_next = __ldg(lut_row + t + 1);
         const int ks = t % KST;
         mbar_wait(k_empty + ks, ((t / KST) & 1) ^ 1);
+#ifdef SPARGE_ABL_NOLOAD   // timing ablation only (wrong results): loads for the first ring pass only
+        if (t >= 4) {
+          mbar_arrive(k_full + ks);
+          mbar_wait(v_empty + t % VST, ((t / VST) & 1) ^ 1);
+          mbar_arrive(v_full + t % VST);
+          continue;
+        }
+#endif
         mbar_arrive_expect_tx(k_full + ks, L::K_BYTES);
         if (QK16) {
 #pragma unroll
@@ -401,6 +468,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       // (kind::f8f6f4 with E4M3 A/B and fp32 D has the f16 field values)
       constexpr uint32_t IDESC_PV = (F16 || PV8) ? idesc_f16(BQ, D) : idesc_bf16(BQ, D);
       const uint64_t dQ = umma_desc_kmajor(smem_u32(sQ), L::ROW_BYTES_QK);
+      constexpr uint32_t IDESC_BIAS = idesc_bf16(BQ, BK);
+      const uint64_t dCA = umma_desc_noswz(smem_u32(smem + L::OFF_CA), 128, 256);
+      const uint64_t dCB = umma_desc_noswz(smem_u32(smem + L::OFF_CB), 128, 256);
       unsigned long long issued = 0;
       mbar_wait(q_full, 0);
       tc_fence_after();
@@ -423,6 +493,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
+#ifdef SPARGE_ABL_NOPV   // timing ablation only (wrong results): one P~V MMA instead of four
+              if (kk == 0)
+#endif
               mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
           }
           ++issued;
@@ -447,9 +520,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             mma_f16(tS0 + sb * BK, dQ + (((kk >> 2) * L::Q_ATOM + (kk & 3) * 32) >> 4),
                     dK + (((kk >> 2) * L::K_ATOM + (kk & 3) * 32) >> 4), IDESC_QK, kk > 0 ? 1u : 0u);
         } else {
+          if (L::BIAS)   // S := 1.5*2^23 (fp32 bits), then += acc as int32
+            mma_f16(tS0 + sb * BK, dCA, dCB, IDESC_BIAS, 0u);
 #pragma unroll
           for (int kk = 0; kk < D / 32; ++kk)       // K = 32 per kind::i8 MMA (32 B)
-            mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, kk > 0 ? 1u : 0u);
+            mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, (L::BIAS || kk > 0) ? 1u : 0u);
         }
         tc_commit(s_full + sb);
         tc_commit(k_empty + ks);
@@ -466,7 +541,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     const int row_g = i * BQ + r;
     const bool row_valid = row_g < p.N;
     const bool tile_tail = (i * BQ + BQ > p.N);
-    constexpr int kMaskedBits = QK16 ? static_cast<int>(0xFF800000u) : INT_MIN;   // -inf / INT_MIN
+    using SB = SBits<QK16, L::BIAS>;
+    constexpr int kMaskedBits = SB::kMasked;   // -inf / INT_MIN / 0 (bias MMA)
     {
       uint32_t z[32];
 #pragma unroll
@@ -510,6 +586,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       const int sb = t & 1;
       const uint32_t tS = tS0 + sb * BK + lane_base;
       int32_t a[BK];
+      uint32_t pw[BK / 2];
       float c = 0.f;
       bool need_mask = false, compute = false, need = false, rescale_o = false;
       float alpha = 1.f;
@@ -526,6 +603,16 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 
         PT_MARK(0);
         mbar_wait(s_full + sb, (t >> 1) & 1);
+#ifdef SPARGE_ABL_NOSOFT   // timing ablation only (wrong results): MMA/sync pipeline floor
+        tc_fence_after();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + quad)), "r"(1u) : "memory");
+          mbar_arrive(p_full + sb);
+        }
+        continue;
+#endif
         PT_MARK(1);
         tc_fence_after();
         tmem_ld32(tS, reinterpret_cast<uint32_t*>(a));
@@ -542,38 +629,61 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           for (int k = 0; k < BK; ++k)
             if (!row_valid || k0 + k > kmax) a[k] = kMaskedBits;
         }
-        float m_loc;
-        bool row_has;
-        if (QK16) {
-          // fp32 row max of S (masked entries -inf), eight chains
-          const float* af = reinterpret_cast<const float*>(a);
-          float f8[8];
+        // row max m_local (Alg. 1 l.14)
+        auto row_max = [&](float& m_loc, bool& row_has) {
+          if (QK16) {
+            // fp32 row max of S (masked entries -inf), eight chains
+            const float* af = reinterpret_cast<const float*>(a);
+            float f8[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) f8[u] = fmaxf(af[u], af[u + 8]);
+            for (int u = 0; u < 8; ++u) f8[u] = fmaxf(af[u], af[u + 8]);
 #pragma unroll
-          for (int k = 16; k < BK; k += 16)
+            for (int k = 16; k < BK; k += 16)
 #pragma unroll
-            for (int u = 0; u < 8; ++u) f8[u] = fmaxf(f8[u], fmaxf(af[k + u], af[k + 8 + u]));
-          const float mxf = fmaxf(fmaxf(fmaxf(f8[0], f8[1]), fmaxf(f8[2], f8[3])),
-                                  fmaxf(fmaxf(f8[4], f8[5]), fmaxf(f8[6], f8[7])));
-          row_has = mxf > -INFINITY;
-          m_loc = row_has ? mxf * c : -INFINITY;
+              for (int u = 0; u < 8; ++u) f8[u] = fmaxf(f8[u], fmaxf(af[k + u], af[k + 8 + u]));
+            const float mxf = fmaxf(fmaxf(fmaxf(f8[0], f8[1]), fmaxf(f8[2], f8[3])),
+                                    fmaxf(fmaxf(f8[4], f8[5]), fmaxf(f8[6], f8[7])));
+            row_has = mxf > -INFINITY;
+            m_loc = row_has ? mxf * c : -INFINITY;
+          } else {
+            // integer-domain row max over the int32 accumulators, or over the
+            // positive fp32 bits 1.5*2^23 + acc (bias MMA): both monotone in
+            // acc, and the dequant scale c > 0; eight independent chains
+            int m8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) m8[u] = max(a[u], a[u + 8]);
+#pragma unroll
+            for (int k = 16; k < BK; k += 16)
+#pragma unroll
+              for (int u = 0; u < 8; ++u) m8[u] = max(m8[u], max(a[k + u], a[k + 8 + u]));
+#ifdef SPARGE_ABL_NOMAX   // timing ablation only (wrong results): no max tree
+            const int mx = max(a[0], a[63]);
+#else
+            const int mx = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])),
+                               max(max(m8[4], m8[5]), max(m8[6], m8[7])));
+#endif
+            // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32
+            // through the magic constant (I2F runs on the slow XU pipe)
+            row_has = mx != kMaskedBits;
+            m_loc = row_has ? (__int_as_float(mx + SB::kAdd) - kMagicF) * c : -INFINITY;
+          }
+        };
+        // PV8: P~' = 2^7 P~ (E4M3 range and precision; l carries the same
+        // factor, so O = acc * s_c / l needs no extra scale)
+        constexpr float kPvShift = PV8 ? 7.0f : 0.0f;
+        float m_loc, rsum = 0.f;
+        bool row_has, have_exps = false;
+        if (kSpec && !need_mask) {
+          // Speculative P~ with the current reference max: with the lazy
+          // reference (R22) it stays put on almost every tile, so the exps
+          // need not wait for the row max -- the max tree and the exps form
+          // one basic block and interleave.  A fresh row (reference -inf)
+          // yields inf here and is recomputed below.
+          exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
+          row_max(m_loc, row_has);
+          have_exps = true;
         } else {
-          // integer-domain row max (monotone: the dequant scale c > 0), eight
-          // independent chains
-          int m8[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) m8[u] = max(a[u], a[u + 8]);
-#pragma unroll
-          for (int k = 16; k < BK; k += 16)
-#pragma unroll
-            for (int u = 0; u < 8; ++u) m8[u] = max(m8[u], max(a[k + u], a[k + 8 + u]));
-          const int mx = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])),
-                             max(max(m8[4], m8[5]), max(m8[6], m8[7])));
-          // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32
-          // through the magic constant (I2F runs on the slow XU pipe)
-          row_has = mx != INT_MIN;
-          m_loc = row_has ? (__int_as_float(mx + kMagic) - kMagicF) * c : -INFINITY;
+          row_max(m_loc, row_has);
         }
         const float m_new = fmaxf(m_true, m_loc);
         // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
@@ -581,6 +691,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         // lazy rescale (R22): move the reference max only when it lags the
         // true max by more than the threshold (always when it is -inf)
         need = compute && (m_new > m_ref + kRefThreshold);
+        const bool redo = __any_sync(0xffffffffu, need) || !have_exps;
         rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
         if (need) {
           alpha = ex2_approx(m_ref - m_new);   // 0 when m_ref = -inf (l, O are 0 then)
@@ -589,18 +700,13 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         }
         m_true = m_new;
         PT_MARK(2);
-      }
 
-      if (PP) named_bar_sync(my_bar, 64);
-      // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ ----
-      uint32_t pw[BK / 2];
-      {
-        float rsum;
-        // PV8: P~' = 2^7 P~ (E4M3 range and precision; l carries the same
-        // factor, so O = acc * s_c / l needs no extra scale)
-        const float mr = PV8 ? m_ref - 7.0f : m_ref;
-        if (need_mask) exps64<true, F16, QK16, PV8>(a, c, mr, pw, rsum);
-        else exps64<false, F16, QK16, PV8>(a, c, mr, pw, rsum);
+        if (PP) named_bar_sync(my_bar, 64);
+        // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ (l.13) ----
+        if (redo) {
+          if (need_mask || kSpec) exps64<true, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
+          else exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
+        }
         l += rsum;           // R9: skipped groups still add their mass to l
       }
       if (PP && !(g == 1 && t == n_iter - 1)) named_bar_arrive(other_bar, 64);

@@ -29,13 +29,25 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // Block until the phase with parity `parity` of `bar` has completed.  The
 // suspend-time hint lets the waiting warp sleep in hardware instead of
 // re-issuing try_wait (spinning warps steal issue slots from the softmax).
+#ifndef SPARGE_WAIT_HINT
+#define SPARGE_WAIT_HINT 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SPARGE_WAIT_HINT
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}"
       ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u) : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}"
+      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ TMA
@@ -163,6 +175,18 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, uint32_
   desc |= sbo << 32;
   desc |= 1ull << 46;
   desc |= layout << 61;
+  return desc;
+}
+
+// SWIZZLE_NONE (layout 0) K-major descriptor: 8-row x 16-B core matrices,
+// `lbo` bytes between core matrices adjacent in K, `sbo` between those
+// adjacent in M/N.
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t desc = 0;
+  desc |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  desc |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  desc |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  desc |= 1ull << 46;
   return desc;
 }
 
