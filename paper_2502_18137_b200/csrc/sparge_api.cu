@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -47,6 +49,21 @@ size_t round256(size_t x) { return (x + 255) / 256 * 256; }
 size_t vt_bytes(const sparge_shape* s) {
   const size_t eb = s->pv_dtype == SPARGE_PV_FP8_E4M3 ? 1 : 2;
   return round256(static_cast<size_t>(s->B) * s->Hkv * s->d * n_pad_of(s) * eb);
+}
+int64_t n_items(const sparge_shape* s) {
+  return static_cast<int64_t>(s->B) * s->Hq * ((s->N + 127) / 128);
+}
+// LPT launch order of the attention CTAs (k_order.cu)
+// (the list, then the k_order scratch: cut value and per-group offsets)
+size_t order_bytes(const sparge_shape* s) {
+  return round256(static_cast<size_t>(n_items(s)) * 4) + round256(static_cast<size_t>(n_items(s) + 2) * 4);
+}
+// Scheduling knobs of k_order (debug overrides; defaults measured on B200):
+// the L2 budget for one group's K^ + V^T and the number of longest items
+// launched first.
+int order_env(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
 }
 size_t chan_bytes(const sparge_shape* s) {
   return round256(static_cast<size_t>(s->B) * s->Hkv * s->d * 4);
@@ -149,7 +166,7 @@ int sparge_predict_mask(const sparge_shape* shape, const double* q_pooled, const
 size_t sparge_attn_workspace(const sparge_shape* shape) {
   if (!shape_ok(shape)) return 0;
   const size_t extra = shape->pv_dtype == SPARGE_PV_FP8_E4M3 ? 2 * chan_bytes(shape) : 0;
-  return kStatusBytes + vt_bytes(shape) + extra;
+  return kStatusBytes + vt_bytes(shape) + extra + order_bytes(shape);
 }
 
 int sparge_attn_fwd(const sparge_shape* shape, const void* qq, const float* dq,
@@ -187,6 +204,8 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
   void* vt = ws + kStatusBytes;
   unsigned int* amax_bits = reinterpret_cast<unsigned int*>(ws + kStatusBytes + vt_bytes(shape));
   float* v_scale = reinterpret_cast<float*>(ws + kStatusBytes + vt_bytes(shape) + chan_bytes(shape));
+  int32_t* order = reinterpret_cast<int32_t*>(
+      ws + kStatusBytes + vt_bytes(shape) + (pv8 ? 2 * chan_bytes(shape) : 0));
 
   cudaError_t e = cudaSuccess;
   if (!(flags & SPARGE_ATTN_SKIP_VPREP)) {
@@ -223,8 +242,23 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
                        d * n_pad * 2, 64, s.d, CU_TENSOR_MAP_SWIZZLE_128B)))
     return SPARGE_ECUDA;
 
+  // launch order: the longest items first, then groups of kv-heads whose
+  // K^ + V^T fit the L2 budget, each longest first (k_order.cu)
+  static const int budget_mb = order_env("SPARGE_ORDER_BUDGET_MB", 48);
+  static const int n_long = order_env("SPARGE_ORDER_LONG", 296);
+  const int64_t kv_head_bytes = static_cast<int64_t>(n_pad) * s.d * ((qk16 ? 2 : 1) + (pv8 ? 1 : 2));
+  // groups of equal size: ceil(kv-heads / groups) kv-heads each
+  const int64_t kv_heads = static_cast<int64_t>(s.B) * s.Hkv;
+  const int64_t kv_fit = std::max<int64_t>(1, (static_cast<int64_t>(budget_mb) << 20) / kv_head_bytes);
+  const int64_t n_groups = (kv_heads + kv_fit - 1) / kv_fit;
+  const int64_t kv_per_group = (kv_heads + n_groups - 1) / n_groups;
+  const int64_t per_group = kv_per_group * (s.Hq / s.Hkv) * ((s.N + 127) / 128);
+  const int n_it = static_cast<int>(n_items(shape));
+  e = launch_order(cnt, n_it, (s.N + 63) / 64, static_cast<int>(std::min<int64_t>(per_group, n_it)),
+                   n_long, order, order + round256(static_cast<size_t>(n_it) * 4) / 4, st);
+  if (e != cudaSuccess) return SPARGE_ECUDA;
   e = launch_attn(s, mq, mk, mv, dq, dk, lut, cnt, lambda, perm, o, o_str, counters, status,
-                  pv8 ? v_scale : nullptr, st);
+                  pv8 ? v_scale : nullptr, order, st);
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
 }
 

@@ -32,9 +32,17 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
                         const int32_t* lut, const int32_t* cnt, float lambda,
                         const int32_t* perm, void* o, sparge_strides o_str,
                         uint64_t* counters, unsigned int* status, const float* v_scale,
-                        cudaStream_t stream);
+                        const int32_t* order, cudaStream_t stream);
 
 int attn_smem_bytes(int d, int qk16);
+
+// Launch order of the attention work items (b * Hq + h) * T_m + i: the
+// n_long items with the largest cnt first, then groups of per_group
+// consecutive items, each by descending cnt (k_order.cu; scheduling only).
+// meta: order_meta_ints(n, per_group) int32 of scratch.
+size_t order_meta_ints(int n, int per_group);
+cudaError_t launch_order(const int32_t* cnt, int n, int tn, int per_group, int n_long,
+                         int32_t* order, int32_t* meta, cudaStream_t stream);
 
 constexpr int kL1Blocks = (SPARGE_L1_OUT_DOUBLES - 2) / 2;
 cudaError_t launch_l1_sums(const void* o, const void* o_ref, int f16, int64_t n, double* out,

@@ -11,35 +11,30 @@
 //        O[I_w] = e^{m - m_new} O[I_w] + P~[I_w] V_j  line 16
 //   O_i = O / l                                       line 19
 //
-// sm_100a design.  A query-tile GROUP = 4 softmax warps + 1 TMA producer
-// warp + 1 MMA warp, 256 TMEM columns (S0 | S1, 64 cols each | O, d cols) and
-// its own K^ / V^T smem rings.  Default: one group per CTA, two CTAs per SM
-// (SPARGE_PAIR=1, an experiment: two groups per CTA, 384 threads, 512 TMEM
-// columns, one CTA per SM).
-//   producer  Q^ once, then K^_j (4-stage ring) and V^T_j (3-stage ring) for
-//             every kept j; SWIZZLE_128B/64B tiles.
-//   MMA       one thread: tcgen05.mma kind::i8 Q^K^^T -> S[t%2] (kind::f16
-//             for the unquantised f1 kernel), then kind::f16 P~ V -> O with
-//             P~ read from TMEM (TS form).  QK(t) is issued right after
-//             P~V(t-2) (in-order tensor pipe).  The P~V MMA is skipped when
-//             all four row groups vote to skip (their P~ rows are zero
-//             otherwise: exact).
+// sm_100a design (v4, "pair" iterations).  One CTA = 4 softmax warps + 1 TMA
+// producer warp + 1 MMA warp, two CTAs per SM, 256 TMEM columns per CTA:
+// S (128 columns: two 64-key tiles side by side) | O (d columns).
+// The kept tiles are processed two at a time (a PAIR, tiles 2p and 2p+1 of
+// the LUT), so every synchronisation round trip between the softmax warps
+// and the MMA warp carries two tiles of tensor work (ablations, profiles/
+// r01s2/attn_ablations.md: with one 64-key tile per round trip the MMA chain
+// alone left the tensor pipe 36 % idle).  Alg. 1 stays tile-sequential: the
+// two tiles keep their own row maxima, gate votes and P~V MMAs.
+//   producer  Q^ once, then K^_t (ring of KST slots; the two tiles of a pair
+//             land in adjacent slots, i.e. one 128-row K-major operand) and
+//             V^T_t (ring of VST slots) for every kept tile.
+//   MMA       one thread.  Pair p: S := 1.5*2^23 (bias MMA, INT8 only), then
+//             kind::i8 Q^ K^^T for both tiles at once (N = 128) -> S; after
+//             the softmax hands P~ back (p_full): kind::f16 P~ V per tile
+//             with P~ read from TMEM (TS form), skipped when all four gate
+//             groups vote to skip that tile.  QK(p+1) is issued right after
+//             the P~V MMAs of pair p (in-order tensor pipe: P~ aliases S).
 //   softmax   thread r owns row r == TMEM lane r; warp w is the gate group
-//             I_w (rows 32w..32w+31).  exp2 domain (lambda compared as
-//             lambda*log2e); the gate max is a warp vote (max_r gap_r >
-//             lambda <=> any_r gap_r > lambda); integer row max; exact
-//             int->fp32 via the 1.5*2^23 magic constant folded into the FFMA
-//             bias (R23); packed f32x2 arithmetic; 1 pair in 8 of the
-//             exponentials on the FMA pipe (exp2_poly2); P~ (16-bit) written
-//             back into the first 32 columns of its own S buffer; lazy O
-//             rescale (R22: the reference max moves only when the true max
-//             grows by > 8 in log2 units; O/l is invariant to the reference,
-//             the gate always uses the true running max).  With two groups
-//             the exp bursts of the two warps sharing an SMSP alternate
-//             (named-barrier ping-pong), so the MUFU stays busy while the
-//             other warp does its per-tile bookkeeping (measured: no gain).
-//   (profiles/experiments/k_attn_v3_splitrow_speculative.cu: a variant with
-//   rows split over 8 softmax warps -- correct, but slower at 96 registers.)
+//             I_w.  Per pair: both tiles' row maxima (integer domain), the
+//             two gate votes in Alg. 1 order, one reference max for the pair
+//             (lazy, R22), exp2 with one FFMA per pair of elements (R23),
+//             P~ (16-bit or E4M3) written over the first columns of its own
+//             tile in S, one arrive.
 #include <cuda.h>
 #include <cstdint>
 #include <climits>
@@ -79,7 +74,11 @@ namespace {
 
 constexpr int BQ = 128;
 constexpr int BK = 64;
-constexpr int NSOFT = 4;      // softmax warps per query tile: one per TMEM lane quadrant
+constexpr int NSOFT = 4;      // softmax warps per group: one per TMEM lane quadrant
+constexpr int NG = 2;         // query-tile groups per CTA (one CTA per SM)
+constexpr int THREADS = (NG * NSOFT + NG + 1) * 32;
+constexpr int WARP_LOAD0 = NG * NSOFT;       // producer of group g: WARP_LOAD0 + g
+constexpr int WARP_MMA = WARP_LOAD0 + NG;    // one MMA issuer for both groups
 #ifndef SPARGE_RESCALE_THR
 #define SPARGE_RESCALE_THR 8
 #endif
@@ -96,47 +95,11 @@ constexpr float kMagicF = 12582912.0f;
 #endif
 constexpr int kPolyEvery = SPARGE_POLY_EVERY;   // one pair in kPolyEvery uses exp2_poly2 (0: none)
 
-// SPARGE_PAIR=1 (experiment, off): one CTA per SM runs two query tiles
-// (NG = 2 groups, each with its own 4 softmax warps, producer warp, MMA warp,
-// smem rings and 256 TMEM columns), optionally with a ping-pong hand-off of
-// the exp bursts between the two warps that share an SMSP (SPARGE_PINGPONG).
-// Measured on Llama 32K: 4.26 ms with ping-pong, 4.23 ms without, vs 3.88 ms
-// for the default of one tile per CTA and two CTAs per SM -- the MUFU
-// contention between co-resident exp bursts is not what limits the softmax.
-#ifndef SPARGE_PAIR
-#define SPARGE_PAIR 0
-#endif
-constexpr bool kPairs = SPARGE_PAIR != 0;
-#ifndef SPARGE_PINGPONG
-#define SPARGE_PINGPONG 1
-#endif
-constexpr bool kPingPong = SPARGE_PINGPONG != 0;
-
-// SPARGE_SPEC (experiment, off: measured slower on Llama/Mochi/CogVideoX):
-// interior tiles compute P~ with the current
-// reference max before the row max is known (see the softmax loop).
-#ifndef SPARGE_SPEC
-#define SPARGE_SPEC 0
-#endif
-constexpr bool kSpec = SPARGE_SPEC != 0 && !kPairs;
-
-template <int NG>
-struct Roles {
-  static constexpr int SOFT = NSOFT * NG;        // softmax warps 4g .. 4g+3
-  static constexpr int LOAD0 = SOFT;             // TMA producer of group g: LOAD0 + g
-  static constexpr int MMA0 = SOFT + NG;         // MMA issuer of group g: MMA0 + g
-  static constexpr int THREADS = (SOFT + 2 * NG) * 32;
-};
-
-// Shared-memory plan of one query-tile group.  QK16 = the unquantised f1
-// kernel (16-bit Q, K tiles stored as d/64 SWIZZLE_128B K-atoms of 128 B
-// rows); with d = 128 its rings shrink to 2 + 2 stages so that two groups
-// still fit on an SM.
-// SPARGE_BIAS_MMA (INT8 QK): before the kind::i8 MMAs of a tile, one
-// kind::f16 MMA (M128 N64 K16, constant operands 1.0 x 1.5*2^19 summed over
-// K = 16) writes the fp32 value 1.5*2^23 into every S accumulator; the i8
-// MMAs then accumulate onto those bits as int32, so S leaves the tensor core
-// as bits(1.5*2^23 + acc) -- the exact fp32 value 1.5*2^23 + acc (R23)
+// SPARGE_BIAS_MMA (INT8 QK): before the kind::i8 MMAs of a pair, one
+// kind::f16 MMA (M128 N<=128 K16, constant operands 1.0 x 1.5*2^19 summed
+// over K = 16) writes the fp32 value 1.5*2^23 into every S accumulator; the
+// i8 MMAs then accumulate onto those bits as int32, so S leaves the tensor
+// core as bits(1.5*2^23 + acc) -- the exact fp32 value 1.5*2^23 + acc (R23)
 // without a per-element integer add in the softmax warps.
 #ifndef SPARGE_BIAS_MMA
 #define SPARGE_BIAS_MMA 1
@@ -145,33 +108,38 @@ constexpr bool kBiasMma = SPARGE_BIAS_MMA != 0;
 constexpr uint16_t kBf16One = 0x3F80;        // bf16 1.0
 constexpr uint16_t kBf16MagicPart = 0x4940;  // bf16 786432 = 1.5*2^19 (x 16 = 1.5*2^23)
 
+// Shared-memory plan.  QK16 = the unquantised f1 kernel (16-bit Q, K tiles
+// stored as d/64 SWIZZLE_128B K-atoms of 128-B rows); with d = 128 its rings
+// shrink to 2 + 2 slots so that two CTAs still fit on an SM.  KST is even:
+// the two tiles of a pair occupy slots (2q, 2q+1), adjacent in memory.
 template <int D, bool QK16, bool PV8 = false>
 struct Smem {
   static constexpr int EB = QK16 ? 2 : 1;       // bytes per Q/K element
-  static constexpr int KST = (QK16 && D == 128) ? 2 : 4;   // K stages
-  static constexpr int VST = (QK16 && D == 128) ? 2 : (PV8 ? 4 : 3);   // V^T stages
+  static constexpr int KST = (QK16 && D == 128) ? 2 : 4;
+  static constexpr int VST = (QK16 && D == 128) ? 2 : (PV8 ? 4 : 3);
   static constexpr int Q_BYTES = BQ * D * EB;
   static constexpr int K_BYTES = BK * D * EB;
   static constexpr int V_BYTES = D * BK * (PV8 ? 1 : 2);    // V^T tile, 16-bit or e4m3
   static constexpr bool BIAS = kBiasMma && !QK16;
-  // constant bias-MMA operands: A 128 x 16 bf16 ones, B 64 x 16 bf16 1.5*2^19
+  // constant bias-MMA operands: A 128 x 16 bf16 ones, B 128 x 16 bf16 1.5*2^19
   static constexpr int CA_BYTES = BIAS ? BQ * 16 * 2 : 0;
-  static constexpr int CB_BYTES = BIAS ? BK * 16 * 2 : 0;
+  static constexpr int CB_BYTES = BIAS ? 2 * BK * 16 * 2 : 0;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * K_BYTES;
   static constexpr int OFF_CA = OFF_V + VST * V_BYTES;
   static constexpr int OFF_CB = OFF_CA + CA_BYTES;
   static constexpr int OFF_BAR = OFF_CB + CB_BYTES;
-  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 3;
+  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 3;
   static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;    // [0] TMEM base, [1..8] pv flags
   static constexpr int TOTAL = OFF_MISC + 64;
-  static constexpr int GROUP = (TOTAL + 1023) / 1024 * 1024;
+  static constexpr int BYTES = (TOTAL + 1023) / 1024 * 1024;
   // INT8: one K-atom of D bytes per row (128 -> SW128, 64 -> SW64); 16-bit:
   // 128-B atoms, the second (d = 128) BQ*128 / BK*128 bytes after the first
   static constexpr int ROW_BYTES_QK = QK16 ? 128 : D;
   static constexpr int Q_ATOM = BQ * 128, K_ATOM = BK * 128;
-  static_assert(2 * GROUP + 1024 <= 227 * 1024, "two groups must fit one SM");
+  static_assert(KST % 2 == 0, "pairs need adjacent K slots");
+  static_assert(NG * BYTES + 1024 <= 227 * 1024, "both groups must fit one CTA");
 };
 
 struct AttnParams {
@@ -185,7 +153,6 @@ struct AttnParams {
   unsigned long long* counters;
   unsigned int* status;
   const float* v_scale;   // PV8: per-(b, hkv, channel) dequant scale s_c [B*Hkv, D]
-  const int32_t* order;   // work items (bhq * T_m + i) by descending cnt (k_order, NG = 1)
   float lam2;         // lambda * log2(e)
   float scale_log2;   // log2(e) / sqrt(d)
   int N, T_m, T_n, Hq, Hkv, group;
@@ -295,11 +262,7 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
     if (!MASKED && kPolyEvery > 0 && ((k >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
       e2 = exp2_poly2(x2);
     else
-#ifdef SPARGE_ABL_NOEXP   // timing ablation only (wrong results): no MUFU
-      e2 = fma2(x2, pk(1e-3f, 1e-3f), pk(1.f, 1.f));
-#else
       e2 = pk(ex2_approx(lo_f(x2)), ex2_approx(hi_f(x2)));
-#endif
     if (MASKED) {
       const float e0 = (a[k] == kMaskedBits || !row_live) ? 0.f : lo_f(e2);
       const float e1 = (a[k + 1] == kMaskedBits || !row_live) ? 0.f : hi_f(e2);
@@ -318,8 +281,8 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
   sum = lo_f(rs) + hi_f(rs);
 }
 
-template <int D, bool CAUSAL, bool F16, bool QK16, int NG, bool PV8>
-__global__ void __launch_bounds__(Roles<NG>::THREADS, 2 / NG)
+template <int D, bool CAUSAL, bool F16, bool QK16, bool PV8>
+__global__ void __launch_bounds__(THREADS, 1)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
   using L = Smem<D, QK16, PV8>;
@@ -334,54 +297,60 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   // FP8 P~ (f4) is rounded relative to the reference max: rescale eagerly so
   // the reference is the true running max (R27), as the oracle's P~ = e^{S-m}
   constexpr float kRefThreshold = PV8 ? 0.0f : (F16 ? kRescaleThresholdF16 : kRescaleThreshold);
-  using R = Roles<NG>;
   constexpr int KST = L::KST, VST = L::VST;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem0 = reinterpret_cast<unsigned char*>(
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   const int warp = __shfl_sync(0xffffffffu, warp_id(), 0), lane = lane_id();
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem0 + L::OFF_MISC);   // group 0's
-  // NG = 1: this CTA's work item comes from the LPT list of k_order (the
-  // items with the most kept blocks launch first); NG = 2 (experiment): two
-  // query tiles of head blockIdx.y
-  int bhq = static_cast<int>(blockIdx.y), i_item = 0;
-  if (NG == 1) {
-    const int item = __ldg(p.order + blockIdx.x);
-    bhq = item / p.T_m;
-    i_item = item - bhq * p.T_m;
-  }
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);   // group 0's
+  const int bhq = blockIdx.y;
   const int b = bhq / p.Hq, hq = bhq % p.Hq;
   const int bkv = b * p.Hkv + hq / p.group;
-  // query tile of group gg: u = blockIdx.x * NG + gg in launch order (causal:
-  // longest rows first); u >= T_m (odd T_m, last pair) is an empty group
+  // Group gg handles query tile u = 2 blockIdx.x + gg (causal: longest rows
+  // first); u >= T_m is an empty group.
   auto tile_of = [&](int gg, int& i_out) -> int {
-    if (NG == 1) {
-      i_out = i_item;
-      return p.cnt[static_cast<int64_t>(bhq) * p.T_m + i_item];
-    }
     const int u = static_cast<int>(blockIdx.x) * NG + gg;
-    if (u >= p.T_m) { i_out = p.T_m; return 0; }
+    if (u >= p.T_m) { i_out = p.T_m - 1; return 0; }
     i_out = CAUSAL ? (p.T_m - 1 - u) : u;
     return p.cnt[static_cast<int64_t>(bhq) * p.T_m + i_out];
   };
+  // group of this warp (softmax warps 4g..4g+3, producer WARP_LOAD0 + g; the
+  // MMA warp serves both).  `warp` comes from a shuffle, so g and every
+  // address derived from it are warp-uniform.
+  const int g = warp < WARP_LOAD0 ? (warp >> 2) : (warp < WARP_MMA ? warp - WARP_LOAD0 : 0);
+  int i = 0;
+  const int n_tiles = tile_of(g, i);
+  const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + i;
+  const int n_pairs = (n_tiles + 1) >> 1;
+  const int32_t* lut_row = p.lut + row_id * p.T_n;
+
+  auto gsm = [&](int gg) { return smem + gg * L::BYTES; };
+  unsigned char* sg = gsm(g);
+  int8_t* sQ = reinterpret_cast<int8_t*>(sg + L::OFF_Q);
+  int8_t* sK = reinterpret_cast<int8_t*>(sg + L::OFF_K);
+  unsigned char* sV = sg + L::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sg + L::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + KST;
+  uint64_t* v_full = k_empty + KST;
+  uint64_t* v_empty = v_full + VST;
+  uint64_t* s_full = v_empty + VST;   // QK of the pair done
+  uint64_t* p_full = s_full + 1;      // P~ of the pair in TMEM (4 softmax warps)
+  uint64_t* o_done = p_full + 1;      // last P~V done (epilogue)
+  uint32_t* pv_flag = reinterpret_cast<uint32_t*>(sg + L::OFF_MISC) + 1;   // [2 tiles][4 warps]
 
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int gg = 0; gg < NG; ++gg) {
-      uint64_t* bg = reinterpret_cast<uint64_t*>(smem0 + gg * L::GROUP + L::OFF_BAR);
-      mbar_init(bg, 1);                                                  // q_full
+      uint64_t* bg = reinterpret_cast<uint64_t*>(gsm(gg) + L::OFF_BAR);
+      mbar_init(bg, 1);
       for (int s = 0; s < KST; ++s) { mbar_init(bg + 1 + s, 1); mbar_init(bg + 1 + KST + s, 1); }
-      for (int s = 0; s < VST; ++s) {
-        mbar_init(bg + 1 + 2 * KST + s, 1);
-        mbar_init(bg + 1 + 2 * KST + VST + s, 1);
-      }
-      uint64_t* sf = bg + 1 + 2 * KST + 2 * VST;
-      for (int s = 0; s < 2; ++s) {
-        mbar_init(sf + s, 1);            // s_full
-        mbar_init(sf + 2 + s, NSOFT);    // p_full
-        mbar_init(sf + 4 + s, 1);        // o_done
-      }
+      for (int s = 0; s < VST; ++s) { mbar_init(bg + 1 + 2 * KST + s, 1); mbar_init(bg + 1 + 2 * KST + VST + s, 1); }
+      mbar_init(bg + 1 + 2 * KST + 2 * VST, 1);          // s_full
+      mbar_init(bg + 2 + 2 * KST + 2 * VST, NSOFT);      // p_full
+      mbar_init(bg + 3 + 2 * KST + 2 * VST, 1);          // o_done
     }
     fence_mbar_init();
   }
@@ -392,47 +361,20 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     constexpr uint32_t kParts = kBf16MagicPart | (static_cast<uint32_t>(kBf16MagicPart) << 16);
 #pragma unroll
     for (int gg = 0; gg < NG; ++gg) {
-      uint32_t* cw = reinterpret_cast<uint32_t*>(smem0 + gg * L::GROUP + L::OFF_CA);
+      uint32_t* cw = reinterpret_cast<uint32_t*>(gsm(gg) + L::OFF_CA);
       for (int x = threadIdx.x; x < (L::CA_BYTES + L::CB_BYTES) / 4; x += blockDim.x)
         cw[x] = x < L::CA_BYTES / 4 ? kOnes : kParts;
     }
     fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
   }
-  if (warp == R::MMA0) tmem_alloc<256 * NG>(tmem_base_slot);
+  if (warp == WARP_MMA) tmem_alloc<256 * NG>(tmem_base_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  const uint32_t tS = tmem_base + g * 256, tO = tS + 2 * BK;
 
-  // group of this warp: softmax warps 4g..4g+3, producer LOAD0+g, MMA MMA0+g.
-  // `warp` comes from a shuffle, so the compiler treats it (and g, and every
-  // smem / barrier / TMEM address derived from it) as warp-uniform; one copy
-  // of the code serves both groups (two copies thrash the instruction cache).
-  const int g = (NG == 1) ? 0
-                          : (warp < R::SOFT ? (warp >> 2)
-                                            : (warp < R::MMA0 ? warp - R::LOAD0 : warp - R::MMA0));
-  unsigned char* smem = smem0 + g * L::GROUP;
-  int8_t* sQ = reinterpret_cast<int8_t*>(smem + L::OFF_Q);
-  int8_t* sK = reinterpret_cast<int8_t*>(smem + L::OFF_K);
-  unsigned char* sV = smem + L::OFF_V;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = k_full + KST;
-  uint64_t* v_full = k_empty + KST;
-  uint64_t* v_empty = v_full + VST;
-  uint64_t* s_full = v_empty + VST;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* o_done = p_full + 2;
-  uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC) + 1;       // [2][4]
-  int i = 0, i_other = 0;
-  const int n_tiles = tile_of(g, i);
-  const int n_other = (NG == 2) ? tile_of(g ^ 1, i_other) : 0;
-  const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + min(i, p.T_m - 1);
-  const int32_t* lut_row = p.lut + row_id * p.T_n;
-  const uint32_t tS0 = tmem_base + g * 256, tO = tS0 + 128;
-
-  if (warp >= R::LOAD0 && warp < R::MMA0) {
+  if (warp >= WARP_LOAD0 && warp < WARP_MMA) {
     // ============================ TMA producer ============================
     if (lane == 0 && n_tiles > 0) {
       tma_prefetch_desc(&tmQ);
@@ -451,14 +393,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         if (t + 1 < n_tiles) j_next = __ldg(lut_row + t + 1);
         const int ks = t % KST;
         mbar_wait(k_empty + ks, ((t / KST) & 1) ^ 1);
-#ifdef SPARGE_ABL_NOLOAD   // timing ablation only (wrong results): loads for the first ring pass only
-        if (t >= 4) {
-          mbar_arrive(k_full + ks);
-          mbar_wait(v_empty + t % VST, ((t / VST) & 1) ^ 1);
-          mbar_arrive(v_full + t % VST);
-          continue;
-        }
-#endif
         mbar_arrive_expect_tx(k_full + ks, L::K_BYTES);
         if (QK16) {
 #pragma unroll
@@ -473,78 +407,138 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
       }
     }
-  } else if (warp >= R::MMA0) {
+  } else if (warp == WARP_MMA) {
     // ============================ MMA issuer ==============================
-    if (lane == 0 && n_tiles > 0) {
-      constexpr uint32_t IDESC_QK =
-          QK16 ? (F16 ? idesc_f16(BQ, BK) : idesc_bf16(BQ, BK)) : idesc_i8(BQ, BK);
-      // (kind::f8f6f4 with E4M3 A/B and fp32 D has the f16 field values)
+    // One thread serves both groups in a fixed alternation (QK(A,0), QK(B,0),
+    // then per pair: P~V(A,p), QK(A,p+1), P~V(B,p), QK(B,p+1)), which keeps
+    // the two groups' softmax phases staggered: while one group's softmax
+    // works on its S, the tensor pipe runs the other group's MMAs.
+    if (lane == 0) {
       constexpr uint32_t IDESC_PV = (F16 || PV8) ? idesc_f16(BQ, D) : idesc_bf16(BQ, D);
-      const uint64_t dQ = umma_desc_kmajor(smem_u32(sQ), L::ROW_BYTES_QK);
-      constexpr uint32_t IDESC_BIAS = idesc_bf16(BQ, BK);
-      const uint64_t dCA = umma_desc_noswz(smem_u32(smem + L::OFF_CA), 128, 256);
-      const uint64_t dCB = umma_desc_noswz(smem_u32(smem + L::OFF_CB), 128, 256);
-      unsigned long long issued = 0;
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      auto do_pv = [&](int u) {
-        const int pb = u & 1, vs = u % VST;
-        mbar_wait(p_full + pb, (u >> 1) & 1);
-        mbar_wait(v_full + vs, (u / VST) & 1);
-        tc_fence_after();
-        const bool any = (pv_flag[pb * 4 + 0] | pv_flag[pb * 4 + 1] |
-                          pv_flag[pb * 4 + 2] | pv_flag[pb * 4 + 3]) != 0;
-        if (any) {
-          const uint32_t tP = tS0 + pb * BK;     // P~ 16-bit (32 cols) or e4m3 (16 cols)
-          if (PV8) {
-            // K = 32 e4m3 per kind::f8f6f4 MMA: 8 TMEM cols of P~, 32 B of V^T rows
-            const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 64);
+      int nt[NG], np[NG];
+      int np_max = 0;
 #pragma unroll
-            for (int kk = 0; kk < BK / 32; ++kk)
-              mma_f8_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
-          } else {
-            const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
-#ifdef SPARGE_ABL_NOPV   // timing ablation only (wrong results): one P~V MMA instead of four
-              if (kk == 0)
+      for (int gg = 0; gg < NG; ++gg) {
+        int ii;
+        nt[gg] = tile_of(gg, ii);
+        np[gg] = (nt[gg] + 1) >> 1;
+        np_max = max(np_max, np[gg]);
+      }
+      unsigned long long issued[NG] = {};
+#ifdef SPARGE_PHASE_TIMING
+      long long mw[3] = {0, 0, 0};   // cycles waiting: p_full, k_full, v_full
+      const long long m_start = clock64();
+#define MMA_WAIT(k, bar, par) do { const long long _c0 = clock64(); mbar_wait(bar, par); mw[k] += clock64() - _c0; } while (0)
+#else
+#define MMA_WAIT(k, bar, par) mbar_wait(bar, par)
 #endif
-              mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
-          }
-          ++issued;
-        }
-        tc_commit(v_empty + vs);
-        tc_commit(o_done + pb);
-      };
-      for (int t = 0; t < n_tiles; ++t) {
-        const int ks = t % KST, sb = t & 1;
-        mbar_wait(k_full + ks, (t / KST) & 1);
-        // S[sb] holds P~(t-2), read by P~V(t-2), which this thread issued
-        // before this QK(t): tcgen05.mma from one thread execute in issue
-        // order, so no completion wait is needed (the softmax warps finished
-        // reading S(t-2) before they arrived on p_full(t-2)).
+      auto bar_of = [&](int gg, int k) { return reinterpret_cast<uint64_t*>(gsm(gg) + L::OFF_BAR) + k; };
+      // QK of pair pp of group gg (Alg. 1 l.12)
+      auto issue_qk = [&](int gg, int pp) {
+        unsigned char* sgg = gsm(gg);
+        const uint32_t tSg = tmem_base + gg * 256;
+        const int t0 = 2 * pp;
+        const bool two = t0 + 1 < nt[gg];
+        const int ks = t0 % KST;                     // even: the pair's slots are ks, ks + 1
+        const uint32_t kpar = (t0 / KST) & 1;
+        MMA_WAIT(1, bar_of(gg, 1 + ks), kpar);
+        if (two) MMA_WAIT(1, bar_of(gg, 2 + ks), kpar);
+        // S holds P~ of pair pp-1, read by its P~V MMAs, which this thread
+        // issued before this QK: tcgen05.mma from one thread execute in issue
+        // order.
         tc_fence_after();
-        const uint64_t dK = umma_desc_kmajor(smem_u32(sK + ks * L::K_BYTES), L::ROW_BYTES_QK);
+        const uint64_t dQ = umma_desc_kmajor(smem_u32(sgg + L::OFF_Q), L::ROW_BYTES_QK);
         if (QK16) {
-          // K = 16 per kind::f16 MMA (32 B): 4 steps per 128-B atom, then
-          // the next atom (fp32 S accumulators)
+          // per tile: K = 16 per kind::f16 MMA (32 B), 4 steps per 128-B
+          // atom, then the next atom (fp32 S accumulators)
+          constexpr uint32_t IDESC_QK = F16 ? idesc_f16(BQ, BK) : idesc_bf16(BQ, BK);
+          for (int h = 0; h < (two ? 2 : 1); ++h) {
+            const uint64_t dK = umma_desc_kmajor(smem_u32(sgg + L::OFF_K + (ks + h) * L::K_BYTES), 128);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            mma_f16(tS0 + sb * BK, dQ + (((kk >> 2) * L::Q_ATOM + (kk & 3) * 32) >> 4),
-                    dK + (((kk >> 2) * L::K_ATOM + (kk & 3) * 32) >> 4), IDESC_QK, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_f16(tSg + h * BK, dQ + (((kk >> 2) * L::Q_ATOM + (kk & 3) * 32) >> 4),
+                      dK + (((kk >> 2) * L::K_ATOM + (kk & 3) * 32) >> 4), IDESC_QK, kk > 0 ? 1u : 0u);
+          }
         } else {
+          // both tiles at once: the two K slots are one 128-row operand
+          const uint64_t dK = umma_desc_kmajor(smem_u32(sgg + L::OFF_K + ks * L::K_BYTES), L::ROW_BYTES_QK);
+          const uint32_t idesc_qk = two ? idesc_i8(BQ, 2 * BK) : idesc_i8(BQ, BK);
           if (L::BIAS)   // S := 1.5*2^23 (fp32 bits), then += acc as int32
-            mma_f16(tS0 + sb * BK, dCA, dCB, IDESC_BIAS, 0u);
+            mma_f16(tSg, umma_desc_noswz(smem_u32(sgg + L::OFF_CA), 128, 256),
+                    umma_desc_noswz(smem_u32(sgg + L::OFF_CB), 128, 256),
+                    two ? idesc_bf16(BQ, 2 * BK) : idesc_bf16(BQ, BK), 0u);
 #pragma unroll
           for (int kk = 0; kk < D / 32; ++kk)       // K = 32 per kind::i8 MMA (32 B)
-            mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, (L::BIAS || kk > 0) ? 1u : 0u);
+            mma_i8(tSg, dQ + 2 * kk, dK + 2 * kk, idesc_qk, (L::BIAS || kk > 0) ? 1u : 0u);
         }
-        tc_commit(s_full + sb);
-        tc_commit(k_empty + ks);
-        if (t > 0) do_pv(t - 1);
+        tc_commit(bar_of(gg, 1 + 2 * KST + 2 * VST));          // s_full
+        tc_commit(bar_of(gg, 1 + KST + ks));                   // k_empty
+        if (two) tc_commit(bar_of(gg, 2 + KST + ks));
+      };
+      // P~V of pair pp of group gg, per tile (Alg. 1 l.15-16)
+      auto issue_pv = [&](int gg, int pp) {
+        unsigned char* sgg = gsm(gg);
+        const uint32_t tSg = tmem_base + gg * 256, tOg = tSg + 2 * BK;
+        const uint32_t* fl0 = reinterpret_cast<const uint32_t*>(sgg + L::OFF_MISC) + 1;
+        const int t0 = 2 * pp;
+        const bool two = t0 + 1 < nt[gg];
+        MMA_WAIT(0, bar_of(gg, 2 + 2 * KST + 2 * VST), pp & 1);   // p_full
+        tc_fence_after();
+        for (int h = 0; h < (two ? 2 : 1); ++h) {
+          const int t = t0 + h;
+          const int vs = t % VST;
+          MMA_WAIT(2, bar_of(gg, 1 + 2 * KST + vs), (t / VST) & 1);   // v_full
+          tc_fence_after();
+          const uint32_t* fl = fl0 + h * 4;
+          if ((fl[0] | fl[1] | fl[2] | fl[3]) != 0) {
+            const uint32_t tP = tSg + h * BK;     // P~ 16-bit (32 cols) or e4m3 (16 cols)
+            if (PV8) {
+              // K = 32 e4m3 per kind::f8f6f4 MMA: 8 TMEM cols of P~, 32 B of V^T rows
+              const uint64_t dV = umma_desc_kmajor(smem_u32(sgg + L::OFF_V + vs * L::V_BYTES), 64);
+#pragma unroll
+              for (int kk = 0; kk < BK / 32; ++kk)
+                mma_f8_ts(tOg, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
+            } else {
+              const uint64_t dV = umma_desc_kmajor(smem_u32(sgg + L::OFF_V + vs * L::V_BYTES), 128);
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
+                mma_f16_ts(tOg, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
+            }
+            ++issued[gg];
+          }
+          tc_commit(bar_of(gg, 1 + 2 * KST + VST + vs));    // v_empty
+        }
+      };
+#pragma unroll
+      for (int gg = 0; gg < NG; ++gg) {
+        if (np[gg] > 0) {
+          mbar_wait(bar_of(gg, 0), 0);   // q_full
+          issue_qk(gg, 0);
+        }
       }
-      do_pv(n_tiles - 1);
-      if (p.counters) atomicAdd(p.counters + bhq * 3 + 2, issued);
+      for (int pp = 0; pp < np_max; ++pp) {
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) {
+          if (pp < np[gg]) {
+            issue_pv(gg, pp);
+            if (pp + 1 < np[gg]) issue_qk(gg, pp + 1);
+            else tc_commit(bar_of(gg, 3 + 2 * KST + 2 * VST));   // o_done
+          }
+        }
+      }
+      if (p.counters) {
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg)
+          if (nt[gg] > 0) atomicAdd(p.counters + bhq * 3 + 2, issued[gg]);
+      }
+#undef MMA_WAIT
+#ifdef SPARGE_PHASE_TIMING
+      if (p.phase_clk) {
+        for (int k = 0; k < 3; ++k) atomicAdd(p.phase_clk + 8 + k, static_cast<unsigned long long>(mw[k]));
+        atomicAdd(p.phase_clk + 11, static_cast<unsigned long long>(clock64() - m_start));
+        atomicAdd(p.phase_clk + 12, 1ull);
+      }
+#endif
     }
   } else {
     // ============================ softmax warps ===========================
@@ -552,10 +546,13 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     const int r = quad * 32 + lane;            // row within the tile == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
     const int row_g = i * BQ + r;
-    const bool row_valid = row_g < p.N;
+    // an empty group (u >= T_m, odd T_m) writes nothing
+    const bool group_live = static_cast<int>(blockIdx.x) * NG + g < p.T_m;
+    const bool row_valid = group_live && row_g < p.N;
     const bool tile_tail = (i * BQ + BQ > p.N);
     using SB = SBits<QK16, L::BIAS>;
     constexpr int kMaskedBits = SB::kMasked;   // -inf / INT_MIN / 0 (bias MMA)
+    constexpr float kPvShift = PV8 ? 7.0f : 0.0f;   // P~' = 2^7 P~ in E4M3 (R27)
     {
       uint32_t z[32];
 #pragma unroll
@@ -570,24 +567,74 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     unsigned int slices = 0;
     // Lane u caches j and the dequant scale c = dq*dk*log2e/sqrt(d) of tile
     // 32*chunk + u; they are broadcast with shuffles, so no global load sits
-    // on the per-tile path.  The next chunk's j is loaded at t%32 == 0 and
-    // its dk at t%32 == 16 (by then j has arrived).
+    // on the per-pair path.  The next chunk's j is loaded when a chunk starts
+    // and its dk sixteen tiles later (by then j has arrived).
     int cj = 0, nj = 0;
     float cc_ = 0.f, ndk = 0.f;
     if (lane < n_tiles) {
       cj = __ldg(lut_row + lane);
       cc_ = dq_scale * __ldg(dk_row + cj);
     }
-    // Pair mode (NG = 2): the exp phases of the two warps that share an SMSP
-    // (warp quad of group 0 and of group 1) alternate strictly -- a bar.sync
-    // / bar.arrive hand-off on barriers 1+quad+4g -- so one warp's MUFU burst
-    // overlaps the other's per-tile bookkeeping instead of contending for the
-    // same MUFU.  Both run max(n_0, n_1) hand-off rounds (a finished group
-    // keeps passing the token), group 1 starts by handing the token to group 0.
-    const uint32_t my_bar = 1 + quad + 4 * g, other_bar = 1 + quad + 4 * (g ^ 1);
-    constexpr bool PP = NG == 2 && kPingPong;
-    const int n_iter = PP ? max(n_tiles, n_other) : n_tiles;
-    if (PP && g == 1 && n_iter > 0) named_bar_arrive(other_bar, 64);
+    // boundary tiles: keys >= N, causal keys > query, rows >= N
+    auto needs_mask = [&](int k0) {
+      return tile_tail || (k0 + BK > p.N) || (CAUSAL && (k0 + BK - 1 > i * BQ));
+    };
+    auto apply_mask = [&](int32_t* a, int k0) {
+      const int kmax = CAUSAL ? min(p.N - 1, row_g) : p.N - 1;
+#pragma unroll
+      for (int k = 0; k < BK; ++k)
+        if (!row_valid || k0 + k > kmax) a[k] = kMaskedBits;
+    };
+    // row max m_local of one tile (Alg. 1 l.14)
+    auto row_max = [&](const int32_t* a, float c, float& m_loc, bool& row_has) {
+      if (QK16) {
+        // fp32 row max of S (masked entries -inf), eight chains
+        const float* af = reinterpret_cast<const float*>(a);
+        float f8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f8[u] = fmaxf(af[u], af[u + 8]);
+#pragma unroll
+        for (int k = 16; k < BK; k += 16)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f8[u] = fmaxf(f8[u], fmaxf(af[k + u], af[k + 8 + u]));
+        const float mxf = fmaxf(fmaxf(fmaxf(f8[0], f8[1]), fmaxf(f8[2], f8[3])),
+                                fmaxf(fmaxf(f8[4], f8[5]), fmaxf(f8[6], f8[7])));
+        row_has = mxf > -INFINITY;
+        m_loc = row_has ? mxf * c : -INFINITY;
+      } else {
+        // integer-domain row max over the int32 accumulators, or over the
+        // positive fp32 bits 1.5*2^23 + acc (bias MMA): both monotone in acc,
+        // and the dequant scale c > 0; eight independent chains
+        int m8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = max(a[u], a[u + 8]);
+#pragma unroll
+        for (int k = 16; k < BK; k += 16)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) m8[u] = max(m8[u], max(a[k + u], a[k + 8 + u]));
+        const int mx = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])),
+                           max(max(m8[4], m8[5]), max(m8[6], m8[7])));
+        // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32
+        // through the magic constant (I2F runs on the slow XU pipe)
+        row_has = mx != kMaskedBits;
+        m_loc = row_has ? (__int_as_float(mx + SB::kAdd) - kMagicF) * c : -INFINITY;
+      }
+    };
+    // P~ of one tile: exps, row sum into l (R9: skipped groups still add their
+    // mass), zero rows when the warp skips, store over the tile's S columns
+    auto softmax_tile = [&](const int32_t* a, bool masked, float c, bool compute, uint32_t tcol) {
+      uint32_t pw[BK / 2];
+      float rsum;
+      if (masked) exps64<true, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
+      else exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
+      l += rsum;
+      if (!compute) {
+#pragma unroll
+        for (int k = 0; k < (PV8 ? BK / 4 : BK / 2); ++k) pw[k] = 0u;
+      }
+      if (PV8) tmem_st16(tcol, pw);
+      else tmem_st32(tcol, pw);
+    };
 #ifdef SPARGE_PHASE_TIMING
     long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
     long long ph_last = clock64();
@@ -595,180 +642,113 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 #ifdef SPARGE_CTA_TIMING
     if (threadIdx.x == 0) { CTA_REC(1, gtimer()); CTA_REC(5, n_tiles); }
 #endif
-    for (int t = 0; t < n_tiles; ++t) {
-      const int sb = t & 1;
-      const uint32_t tS = tS0 + sb * BK + lane_base;
-      int32_t a[BK];
-      uint32_t pw[BK / 2];
-      float c = 0.f;
-      bool need_mask = false, compute = false, need = false, rescale_o = false;
-      float alpha = 1.f;
-      {
-        const int tl = t & 31;
-        if (tl == 0) {
-          if (t > 0) { cj = nj; cc_ = dq_scale * ndk; }
-          if (t + 32 + lane < n_tiles) nj = __ldg(lut_row + t + 32 + lane);
-        } else if (tl == 16) {
-          if (t + 16 + lane < n_tiles) ndk = __ldg(dk_row + nj);
-        }
-        const int j = __shfl_sync(0xffffffffu, cj, tl);
-        c = __shfl_sync(0xffffffffu, cc_, tl);
+    const uint32_t tSa = tS + lane_base, tSb = tS + BK + lane_base;
+    for (int pp = 0; pp < n_pairs; ++pp) {
+      const int t0 = 2 * pp;
+      const bool two = t0 + 1 < n_tiles;
+      // ---- LUT entries of the pair ----
+      const int tl = t0 & 31;
+      if (tl == 0) {
+        if (t0 > 0) { cj = nj; cc_ = dq_scale * ndk; }
+        if (t0 + 32 + lane < n_tiles) nj = __ldg(lut_row + t0 + 32 + lane);
+      } else if (tl == 16) {
+        if (t0 + 16 + lane < n_tiles) ndk = __ldg(dk_row + nj);
+      }
+      const int k0a = __shfl_sync(0xffffffffu, cj, tl) * BK;
+      const float ca = __shfl_sync(0xffffffffu, cc_, tl);
+      const int k0b = __shfl_sync(0xffffffffu, cj, tl + 1) * BK;
+      const float cb = __shfl_sync(0xffffffffu, cc_, tl + 1);
+      const bool nma = needs_mask(k0a);
+      const bool nmb = two && needs_mask(k0b);
 
-        PT_MARK(0);
-        mbar_wait(s_full + sb, (t >> 1) & 1);
+      mbar_wait(s_full, pp & 1);
+      tc_fence_after();
 #ifdef SPARGE_ABL_NOSOFT   // timing ablation only (wrong results): MMA/sync pipeline floor
-        tc_fence_after();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + quad)), "r"(1u) : "memory");
-          mbar_arrive(p_full + sb);
-        }
-        continue;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        pv_flag[quad] = 1u;
+        pv_flag[4 + quad] = 1u;
+        mbar_arrive(p_full);
+      }
+      continue;
 #endif
-        PT_MARK(1);
-        tc_fence_after();
-        tmem_ld32(tS, reinterpret_cast<uint32_t*>(a));
-        tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(a) + 32);
+      PT_MARK(0);
+      int32_t a[BK];
+      // ---- tile b: row max only (reloaded for its exps below) ----
+      float mlb = -INFINITY;
+      bool hasb = false;
+      if (two) {
+        tmem_ld32(tSb, reinterpret_cast<uint32_t*>(a));
+        tmem_ld32(tSb + 32, reinterpret_cast<uint32_t*>(a) + 32);
         tmem_wait_ld();
-        PT_MARK(6);
-
-        // ---- masking of boundary tiles: keys >= N, causal keys > query, rows >= N
-        const int k0 = j * BK;
-        need_mask = tile_tail || (k0 + BK > p.N) || (CAUSAL && (k0 + BK - 1 > i * BQ));
-        if (need_mask) {
-          const int kmax = CAUSAL ? min(p.N - 1, row_g) : p.N - 1;
-#pragma unroll
-          for (int k = 0; k < BK; ++k)
-            if (!row_valid || k0 + k > kmax) a[k] = kMaskedBits;
-        }
-        // row max m_local (Alg. 1 l.14)
-        auto row_max = [&](float& m_loc, bool& row_has) {
-          if (QK16) {
-            // fp32 row max of S (masked entries -inf), eight chains
-            const float* af = reinterpret_cast<const float*>(a);
-            float f8[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) f8[u] = fmaxf(af[u], af[u + 8]);
-#pragma unroll
-            for (int k = 16; k < BK; k += 16)
-#pragma unroll
-              for (int u = 0; u < 8; ++u) f8[u] = fmaxf(f8[u], fmaxf(af[k + u], af[k + 8 + u]));
-            const float mxf = fmaxf(fmaxf(fmaxf(f8[0], f8[1]), fmaxf(f8[2], f8[3])),
-                                    fmaxf(fmaxf(f8[4], f8[5]), fmaxf(f8[6], f8[7])));
-            row_has = mxf > -INFINITY;
-            m_loc = row_has ? mxf * c : -INFINITY;
-          } else {
-            // integer-domain row max over the int32 accumulators, or over the
-            // positive fp32 bits 1.5*2^23 + acc (bias MMA): both monotone in
-            // acc, and the dequant scale c > 0; eight independent chains
-            int m8[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) m8[u] = max(a[u], a[u + 8]);
-#pragma unroll
-            for (int k = 16; k < BK; k += 16)
-#pragma unroll
-              for (int u = 0; u < 8; ++u) m8[u] = max(m8[u], max(a[k + u], a[k + 8 + u]));
-#ifdef SPARGE_ABL_NOMAX   // timing ablation only (wrong results): no max tree
-            const int mx = max(a[0], a[63]);
-#else
-            const int mx = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])),
-                               max(max(m8[4], m8[5]), max(m8[6], m8[7])));
-#endif
-            // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32
-            // through the magic constant (I2F runs on the slow XU pipe)
-            row_has = mx != kMaskedBits;
-            m_loc = row_has ? (__int_as_float(mx + SB::kAdd) - kMagicF) * c : -INFINITY;
-          }
-        };
-        // PV8: P~' = 2^7 P~ (E4M3 range and precision; l carries the same
-        // factor, so O = acc * s_c / l needs no extra scale)
-        constexpr float kPvShift = PV8 ? 7.0f : 0.0f;
-        float m_loc, rsum = 0.f;
-        bool row_has, have_exps = false;
-        if (kSpec && !need_mask) {
-          // Speculative P~ with the current reference max: with the lazy
-          // reference (R22) it stays put on almost every tile, so the exps
-          // need not wait for the row max -- the max tree and the exps form
-          // one basic block and interleave.  A fresh row (reference -inf)
-          // yields inf here and is recomputed below.
-          exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
-          row_max(m_loc, row_has);
-          have_exps = true;
-        } else {
-          row_max(m_loc, row_has);
-        }
-        const float m_new = fmaxf(m_true, m_loc);
-        // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
-        compute = __any_sync(0xffffffffu, row_has && (m_loc - m_new > p.lam2));
-        // lazy rescale (R22): move the reference max only when it lags the
-        // true max by more than the threshold (always when it is -inf)
-        need = compute && (m_new > m_ref + kRefThreshold);
-        const bool redo = __any_sync(0xffffffffu, need) || !have_exps;
-        rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
-        if (need) {
-          alpha = ex2_approx(m_ref - m_new);   // 0 when m_ref = -inf (l, O are 0 then)
-          l *= alpha;
-          m_ref = m_new;
-        }
-        m_true = m_new;
-        PT_MARK(2);
-
-        if (PP) named_bar_sync(my_bar, 64);
-        // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ (l.13) ----
-        if (redo) {
-          if (need_mask || kSpec) exps64<true, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
-          else exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
-        }
-        l += rsum;           // R9: skipped groups still add their mass to l
+        if (nmb) apply_mask(a, k0b);
+        row_max(a, cb, mlb, hasb);
       }
-      if (PP && !(g == 1 && t == n_iter - 1)) named_bar_arrive(other_bar, 64);
-
-      {
-        if (!compute) {
-#pragma unroll
-          for (int k = 0; k < (PV8 ? BK / 4 : BK / 2); ++k) pw[k] = 0u;
-        }
-        PT_MARK(4);
-
-        if (rescale_o) {
-          // O rows of this warp hold P~V of earlier tiles: wait for the last
-          // issued P~V, then rescale in TMEM (before p_full(t) releases P~V(t)).
-          if (t >= 1) mbar_wait(o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int cc = 0; cc < D / 32; ++cc) {
-            uint32_t ov[32];
-            tmem_ld32(tO + lane_base + cc * 32, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
-            tmem_st32(tO + lane_base + cc * 32, ov);
-          }
-        }
-        PT_MARK(3);
-
-        // P~(t) overwrites the first 32 columns of S[sb]: S(t) is already in
-        // registers, and QK(t) -- complete, per s_full -- executed after
-        // P~V(t-2), the previous reader of this buffer.
-        if (PV8) tmem_st16(tS, pw);
-        else tmem_st32(tS, pw);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + quad)),
-                       "r"(compute ? 1u : 0u) : "memory");
-          mbar_arrive(p_full + sb);
-        }
-        if (compute) ++slices;
-        PT_MARK(5);
+      PT_MARK(1);
+      // ---- tile a: row max, kept in registers ----
+      tmem_ld32(tSa, reinterpret_cast<uint32_t*>(a));
+      tmem_ld32(tSa + 32, reinterpret_cast<uint32_t*>(a) + 32);
+      tmem_wait_ld();
+      if (nma) apply_mask(a, k0a);
+      float mla;
+      bool hasa;
+      row_max(a, ca, mla, hasa);
+      // ---- gates in Alg. 1 order: tile a, then tile b (l.14-15) ----
+      const float mn0 = fmaxf(m_true, mla);
+      const bool comp0 = __any_sync(0xffffffffu, hasa && (mla - mn0 > p.lam2));
+      const float mn1 = fmaxf(mn0, mlb);
+      const bool comp1 = two && __any_sync(0xffffffffu, hasb && (mlb - mn1 > p.lam2));
+      // one reference for the pair (R22): move it only when a computing tile
+      // pushes the true max more than the threshold above it
+      const bool need = (comp0 || comp1) && (mn1 > m_ref + kRefThreshold);
+      const bool rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
+      float alpha = 1.f;
+      if (need) {
+        alpha = ex2_approx(m_ref - mn1);   // 0 when m_ref = -inf (l, O are 0 then)
+        l *= alpha;
+        m_ref = mn1;
       }
-    }
-    // this group is done: keep passing the token while the other one works
-    for (int t = n_tiles; PP && t < n_iter; ++t) {
-      named_bar_sync(my_bar, 64);
-      if (!(g == 1 && t == n_iter - 1)) named_bar_arrive(other_bar, 64);
+      m_true = mn1;
+      PT_MARK(2);
+      if (rescale_o) {
+        // O rows of this warp hold P~V of earlier pairs, all complete (s_full
+        // of this pair was committed after them): rescale in TMEM before
+        // p_full releases this pair's P~V.
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t ov[32];
+          tmem_ld32(tO + lane_base + cc * 32, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) ov[k] = __float_as_uint(__uint_as_float(ov[k]) * alpha);
+          tmem_st32(tO + lane_base + cc * 32, ov);
+        }
+      }
+      PT_MARK(3);
+      // ---- P~ of tile a, then tile b ----
+      softmax_tile(a, nma, ca, comp0, tSa);
+      PT_MARK(4);
+      if (two) {
+        tmem_ld32(tSb, reinterpret_cast<uint32_t*>(a));
+        tmem_ld32(tSb + 32, reinterpret_cast<uint32_t*>(a) + 32);
+        tmem_wait_ld();
+        if (nmb) apply_mask(a, k0b);
+        softmax_tile(a, nmb, cb, comp1, tSb);
+      }
+      PT_MARK(5);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + quad)),
+                     "r"(comp0 ? 1u : 0u) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + 4 + quad)),
+                     "r"(comp1 ? 1u : 0u) : "memory");
+        mbar_arrive(p_full);
+      }
+      slices += (comp0 ? 1u : 0u) + (comp1 ? 1u : 0u);
+      PT_MARK(6);
     }
 #ifdef SPARGE_PHASE_TIMING
     if (lane == 0 && p.phase_clk)
@@ -781,7 +761,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     if (threadIdx.x == 0) CTA_REC(2, gtimer());
 #endif
     // ---- epilogue: O_i = O / l (line 19), scattered back through perm ----
-    if (n_tiles > 0) mbar_wait(o_done + ((n_tiles - 1) & 1), ((n_tiles - 1) >> 1) & 1);
+    if (n_tiles > 0) mbar_wait(o_done, 0);
     tc_fence_after();
     if (row_valid && !(l > 0.f)) atomicOr(p.status, 1u);
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
@@ -819,7 +799,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == R::MMA0) {
+  if (warp == WARP_MMA) {
     __syncwarp();
     tc_fence_after();
     tmem_dealloc<256 * NG>(tmem_base);
@@ -832,13 +812,12 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 template <int D, bool CAUSAL, bool F16, bool QK16, bool PV8 = false>
 cudaError_t launch_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                      const AttnParams& p, int B, cudaStream_t stream) {
-  constexpr int NG = kPairs ? 2 : 1;
-  auto kern = k_sparse_attn<D, CAUSAL, F16, QK16, NG, PV8>;
-  const int smem = NG * Smem<D, QK16, PV8>::GROUP + 1024;   // + slack for 1024-B alignment
+  auto kern = k_sparse_attn<D, CAUSAL, F16, QK16, PV8>;
+  const int smem = NG * Smem<D, QK16, PV8>::BYTES + 1024;   // + slack for 1024-B alignment
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(NG == 1 ? p.T_m * B * p.Hq : (p.T_m + NG - 1) / NG, NG == 1 ? 1 : B * p.Hq);
-  kern<<<grid, Roles<NG>::THREADS, smem, stream>>>(mq, mk, mv, p);
+  dim3 grid((p.T_m + NG - 1) / NG, B * p.Hq);
+  kern<<<grid, THREADS, smem, stream>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
 
@@ -849,10 +828,9 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
                         const int32_t* lut, const int32_t* cnt, float lambda,
                         const int32_t* perm, void* o, sparge_strides o_str,
                         uint64_t* counters, unsigned int* status, const float* v_scale,
-                        const int32_t* order, cudaStream_t stream) {
+                        cudaStream_t stream) {
   AttnParams p;
   p.v_scale = v_scale;
-  p.order = order;
   p.dq = dq; p.dk = dk; p.lut = lut; p.cnt = cnt; p.perm = perm;
   p.o = static_cast<uint16_t*>(o);
   p.o_sb = o_str.b; p.o_sh = o_str.h; p.o_sn = o_str.n;
@@ -891,9 +869,8 @@ namespace sparge {
 #endif
 
 int attn_smem_bytes(int d, int qk16) {
-  const int ng = kPairs ? 2 : 1;
-  if (qk16) return ng * (d == 128 ? Smem<128, true>::GROUP : Smem<64, true>::GROUP) + 1024;
-  return ng * (d == 128 ? Smem<128, false>::GROUP : Smem<64, false>::GROUP) + 1024;
+  if (qk16) return NG * (d == 128 ? Smem<128, true>::BYTES : Smem<64, true>::BYTES) + 1024;
+  return NG * (d == 128 ? Smem<128, false>::BYTES : Smem<64, false>::BYTES) + 1024;
 }
 
 }  // namespace sparge

@@ -192,3 +192,35 @@ def test_host_pipeline_matches_device_path(lib):
     pipe(qh, kh, vh, oh, 0.9, 0.5, -5.0)
     torch.cuda.synchronize()
     assert torch.equal(oh, o_ref.cpu())
+
+
+def _launch_order(bf, shape):
+    """The attention launch order k_order leaves in the workspace (after the
+    status word and V^T): int32 work items (b*Hq+h)*T_m+i."""
+    B, Hq, Hkv, N, d = shape.B, shape.Hq, shape.Hkv, shape.N, shape.d
+    n_pad = (N + 63) // 64 * 64
+    vt = (B * Hkv * d * n_pad * 2 + 255) // 256 * 256
+    n = B * Hq * ((N + 127) // 128)
+    ws = bf.workspace
+    return ws[256 + vt:256 + vt + 4 * n].view(torch.int32).cpu().numpy()
+
+
+@pytest.mark.parametrize("N,Hq,Hkv,causal", [(8192, 16, 4, True), (6000, 12, 12, False)])
+def test_launch_order_is_longest_first_permutation(lib, N, Hq, Hkv, causal):
+    """Scheduling only (k_order.cu): the launch order is a permutation of the
+    work items that starts with the longest one and consists of at most
+    1 + (number of kv-head groups) non-increasing runs of cnt (the long items,
+    then each group longest first)."""
+    qn, kn, vn = inputs.llm_local(N + 128, N, d=128, Hq=Hq, Hkv=Hkv, gamma=1.5)
+    q, k, v = _dev(qn), _dev(kn), _dev(vn)
+    o, bf = _run(lib, q, k, v, 0.9, 0.5, -5.0, causal)
+    torch.cuda.synchronize()
+    order = _launch_order(bf, bf.shape)
+    cnt = bf.cnt.cpu().numpy().reshape(-1)
+    n = cnt.size
+    assert n > 296
+    assert np.array_equal(np.sort(order), np.arange(n))
+    c = cnt[order]
+    assert c[0] == cnt.max()
+    runs = 1 + int(np.sum(np.diff(c) > 0))
+    assert runs <= 1 + Hkv, runs
