@@ -312,7 +312,7 @@ def run_ours(args):
                         "note": "a0 index build on the host once per shape; the gather is "
                                 "fused into a1 / the V stage and the scatter into a3"},
         "roofline": roofline,
-        "gpu_launches": 5 * K,
+        "gpu_launches": 8 * K,   # per step: quant x2, S^ DMMA, TopCdf, V^T, order x2, attention
         "clocks": clk.summary(),
     }
     if args.profile:

@@ -29,11 +29,12 @@
 //             lambda*log2e); the gate max is a warp vote (max_r gap_r >
 //             lambda <=> any_r gap_r > lambda); integer row max; exact
 //             int->fp32 via the 1.5*2^23 magic constant folded into the FFMA
-//             bias (R23); packed f32x2 arithmetic; 1 pair in 8 of the
-//             exponentials on the FMA pipe (exp2_poly2); P~ (16-bit) written
+//             bias (R23); packed f32x2 arithmetic; all exponentials on the
+//             MUFU (SPARGE_POLY_EVERY=k moves 1 pair in k to the FMA pipe,
+//             exp2_poly2: slower since the MUFU is not the bound); P~ (16-bit) written
 //             back into the first 32 columns of its own S buffer; lazy O
 //             rescale (R22: the reference max moves only when the true max
-//             grows by > 8 in log2 units; O/l is invariant to the reference,
+//             grows by > 16 in log2 units (15 for fp16 P~); O/l is invariant to the reference,
 //             the gate always uses the true running max).  With two groups
 //             the exp bursts of the two warps sharing an SMSP alternate
 //             (named-barrier ping-pong), so the MUFU stays busy while the
@@ -81,7 +82,7 @@ constexpr int BQ = 128;
 constexpr int BK = 64;
 constexpr int NSOFT = 4;      // softmax warps per query tile: one per TMEM lane quadrant
 #ifndef SPARGE_RESCALE_THR
-#define SPARGE_RESCALE_THR 8
+#define SPARGE_RESCALE_THR 16
 #endif
 // lazy-rescale threshold (R22), log2 units: P~ <= 2^thr, which fp16 P~ must
 // hold (max 65504 < 2^16)
@@ -92,7 +93,7 @@ constexpr int kMagic = 0x4B400000;          // bits of 1.5 * 2^23
 constexpr float kMagicF = 12582912.0f;
 
 #ifndef SPARGE_POLY_EVERY
-#define SPARGE_POLY_EVERY 8
+#define SPARGE_POLY_EVERY 0
 #endif
 constexpr int kPolyEvery = SPARGE_POLY_EVERY;   // one pair in kPolyEvery uses exp2_poly2 (0: none)
 
