@@ -515,7 +515,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           ++issued;
         }
         tc_commit(v_empty + vs);
-        tc_commit(o_done + pb);
+        // o_done completes after P~V(n-2) and P~V(n-1) only: the softmax's
+        // rare O rescale at tile t <= n-2 waits on s_full(t+1) instead (QK(t+1)
+        // is issued after P~V(t-1)), the one at tile n-1 and the epilogue on
+        // o_done -- one tcgen05.commit (~44 issue cycles) less per tile
+        if (u + 2 >= n_tiles) tc_commit(o_done);
       };
       for (int t = 0; t < n_tiles; ++t) {
         const int ks = t % KST, sb = t & 1;
@@ -735,7 +739,10 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         if (rescale_o) {
           // O rows of this warp hold P~V of earlier tiles: wait for the last
           // issued P~V, then rescale in TMEM (before p_full(t) releases P~V(t)).
-          if (t >= 1) mbar_wait(o_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
+          if (t >= 1) {
+            if (t + 1 < n_tiles) mbar_wait(s_full + ((t + 1) & 1), ((t + 1) >> 1) & 1);
+            else mbar_wait(o_done, 0);     // completion 0 = P~V(n-2)
+          }
           tc_fence_after();
 #pragma unroll
           for (int cc = 0; cc < D / 32; ++cc) {
@@ -782,7 +789,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     if (threadIdx.x == 0) CTA_REC(2, gtimer());
 #endif
     // ---- epilogue: O_i = O / l (line 19), scattered back through perm ----
-    if (n_tiles > 0) mbar_wait(o_done + ((n_tiles - 1) & 1), ((n_tiles - 1) >> 1) & 1);
+    if (n_tiles > 0) mbar_wait(o_done, n_tiles >= 2 ? 1 : 0);   // P~V(n-1)
     tc_fence_after();
     if (row_valid && !(l > 0.f)) atomicOr(p.status, 1u);
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
@@ -842,6 +849,7 @@ cudaError_t launch_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   kern<<<grid, Roles<NG>::THREADS, smem, stream>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
+
 
 }  // namespace
 

@@ -27,6 +27,18 @@ __device__ __forceinline__ void mma_f16_ts_elect(uint32_t d, uint32_t a, uint64_
                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
                ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
 }
+// four kind::i8 MMAs in ONE asm statement (descriptor steps of 2 = 32 B)
+__device__ __forceinline__ void mma_i8_x4(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile("{\n\t.reg .pred p;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+               "setp.ne.b32 p, 1, 0;\n\t"
+               "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+               "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %3, p;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %3, p;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %3, p;\n\t}"
+               ::"r"(d), "l"(a), "l"(b), "r"(idesc) : "memory");
+}
 template <int MODE>
 __global__ void __launch_bounds__(128) k(unsigned long long* out, int salt) {
   extern __shared__ unsigned char raw[];
@@ -34,11 +46,11 @@ __global__ void __launch_bounds__(128) k(unsigned long long* out, int salt) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 65536);
   uint32_t* slot = reinterpret_cast<uint32_t*>(sm + 65536 + 64);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) { mbar_init(bars, 1); fence_mbar_init(); }
+  if (threadIdx.x == 0) { mbar_init(bars, 1); mbar_init(bars + 1, 1); fence_mbar_init(); }
   if (warp == 0) tmem_alloc<512>(slot);
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tm = *slot;
-  if (MODE >= 8 && warp == 1) {
+  if (MODE >= 8 && MODE < 12 && warp == 1) {
     // converged warp, elect.sync inside the asm
     const uint64_t dQ = umma_desc_kmajor(smem_u32(sm), 128);
     const uint64_t dK = umma_desc_kmajor(smem_u32(sm + 16384), 128);
@@ -63,7 +75,7 @@ __global__ void __launch_bounds__(128) k(unsigned long long* out, int salt) {
     __syncwarp();
     long long t1 = clock64();
     if (lane == 0) out[blockIdx.x] = static_cast<unsigned long long>(t1 - t0);
-  } else if (MODE < 8 && warp == 1 && lane == 0) {
+  } else if ((MODE < 8 || MODE >= 12) && warp == 1 && lane == 0) {
     const uint64_t dQ = umma_desc_kmajor(smem_u32(sm), 128);
     const uint64_t dK = umma_desc_kmajor(smem_u32(sm + 16384), 128);
     const uint64_t dV = umma_desc_kmajor(smem_u32(sm + 32768), 128);
@@ -90,6 +102,16 @@ __global__ void __launch_bounds__(128) k(unsigned long long* out, int salt) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) mma_i8(tm, dQ + 2 * kk, dK + 2 * kk, idesc_i8(128, 64), 1u);
         tc_commit(bars);
+      } else if (MODE == 12) {   // 4 x i8 M64 N8 K32 (tiny: issue-bound)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) mma_i8(tm, dQ + 2 * kk, dK + 2 * kk, idesc_i8(64, 8), 1u);
+      } else if (MODE == 14) {   // 4 x i8 M64 N8 in one asm statement
+        mma_i8_x4(tm, dQ, dK, idesc_i8(64, 8));
+      } else if (MODE == 15) {   // 4 x i8 N64 in one asm statement
+        mma_i8_x4(tm, dQ, dK, idesc_i8(128, 64));
+      } else if (MODE == 13) {   // 4 x commits
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) tc_commit(bars + 1);
       } else if (MODE == 7) {   // 1 x i8 N64, destination varies (2 buffers)
         mma_i8(tm + (it & 1) * 64, dQ, dK, idesc_i8(128, 64), 1u);
       }
@@ -128,5 +150,9 @@ int main() {
   run<9>("[warp+elect] 1x i8 N16 K32 invariant", 1);
   run<10>("[warp+elect] 4x f16 TS N128 K16", 4);
   run<11>("[warp+elect] 4x i8 N64, K slot + D vary", 4);
+  run<12>("4x i8 M64 N8 K32 (tiny)", 4);
+  run<13>("4x tcgen05.commit", 4);
+  run<14>("4x i8 M64 N8 in one asm", 4);
+  run<15>("4x i8 N64 in one asm", 4);
   return 0;
 }
