@@ -20,6 +20,9 @@ __all__ = [
     "f32",
     "block_count",
     "quantize_blocks",
+    "SMOOTH_CHUNK",
+    "smooth_k_mean",
+    "smooth_k",
     "block_mean",
     "cos_sim",
     "block_sims",
@@ -88,6 +91,37 @@ def quantize_blocks(x, b):
         q[i * b:min((i + 1) * b, n)] = qi.astype(np.int8)
         delta[i] = amax / np.float32(127.0)
     return q, delta
+
+
+# --------------------------------------------------------------------------
+# Row f4, K smoothing (SageAttention, footnote P:L44 "SageAttention2"; the
+# paper fixes no arithmetic -- reading R28): K' = K - mean_t K before the
+# INT8 quantisation of line 3.  S' = S - q.mu is a per-query-row constant
+# shift, so softmax, the lambda gate's m_local - m_new and O are unchanged in
+# exact arithmetic; only the INT8 rounding of K improves.  Stage 1 keeps the
+# raw K (R14: P^ is shift-invariant, CosSim is not).
+# --------------------------------------------------------------------------
+SMOOTH_CHUNK = 128
+
+
+def smooth_k_mean(k):
+    """mu = the per-channel token mean of one head's K [N, d], in the fixed
+    summation order of reading R28: fp64, tokens in index order within chunks
+    of SMOOTH_CHUNK tokens (a sequential sum), chunk sums added in chunk
+    order; then / N and rounded to fp32."""
+    k = np.asarray(k, dtype=np.float64)
+    n, d = k.shape
+    total = np.zeros(d)
+    for c0 in range(0, n, SMOOTH_CHUNK):
+        part = np.cumsum(k[c0:min(c0 + SMOOTH_CHUNK, n)], axis=0)[-1]   # sequential
+        total = total + part
+    return (total / n).astype(np.float32)
+
+
+def smooth_k(k, mu):
+    """K' = fl32(K - mu) element-wise (fp32 subtraction, RNE), as fp64."""
+    k32 = np.asarray(k, dtype=np.float64).astype(np.float32)
+    return (k32 - np.asarray(mu, dtype=np.float32)).astype(np.float32).astype(np.float64)
 
 
 # --------------------------------------------------------------------------
@@ -447,16 +481,25 @@ def sparsity_of(qk_exec, pv_slices_exec, live_tiles, cw=4):
 
 
 def spargeattn_head(q, k, v, tau, theta, lam, bq=128, bk=64, cw=4, causal=False,
-                    sim_mode="cosine", quantize=True, pv_round="bf16", qblocks=None):
+                    sim_mode="cosine", quantize=True, pv_round="bf16", qblocks=None,
+                    smooth=False):
     """The whole of Algorithm 1 for one head: stage 1 (lines 3-6) then the
-    sparse loop (lines 7-21).  Returns (O, M, near, counters, quant)."""
+    sparse loop (lines 7-21).  smooth: K smoothing before the INT8
+    quantisation (row f4, R28; stage 1 keeps the raw K, R14) -- True (mu of
+    this k) or the fp32 mu itself.  Returns (O, M, near, counters, quant)."""
     q = np.asarray(q, dtype=np.float64)
     k = np.asarray(k, dtype=np.float64)
     M, near = predict_mask(q, k, tau, theta, bq, bk, causal, sim_mode)
     quant = None
     if quantize:
         Qq, dq = quantize_blocks(q, bq)
-        Kq, dk = quantize_blocks(k, bk)
+        if smooth is not False and smooth is not None:
+            # mu of the head's K in its ORIGINAL token order (R28): passed in
+            # by a caller that permuted k, else computed here
+            mu = smooth_k_mean(k) if smooth is True else np.asarray(smooth, dtype=np.float32)
+            Kq, dk = quantize_blocks(smooth_k(k, mu), bk)
+        else:
+            Kq, dk = quantize_blocks(k, bk)
         quant = (Qq, dq, Kq, dk)
     v_fp8 = fp8_v_quant(v) if pv_round == "fp8" else None
     O, cnt = sparse_attention(q, k, v, M, lam, bq, bk, cw, causal, quant, pv_round, qblocks,

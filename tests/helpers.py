@@ -13,7 +13,7 @@ def bf16_np(t):
 
 
 def oracle_forward(q, k, v, tau, theta, lam, causal=False, perm=None, group=1, qblocks=None,
-                   heads=None, sim_mode="cosine", quantize=True, pv_round="bf16"):
+                   heads=None, sim_mode="cosine", quantize=True, pv_round="bf16", smooth=False):
     """Oracle pipeline on fp64 arrays q [Hq, N, d], k/v [Hkv, N, d] (one batch).
     With perm the sequence is permuted first and O inverse-permuted.
     Returns dict of per-head results."""
@@ -23,11 +23,13 @@ def oracle_forward(q, k, v, tau, theta, lam, causal=False, perm=None, group=1, q
     for h in (range(Hq) if heads is None else heads):
         g = h // group
         qh, kh, vh = q[h], k[g], v[g]
+        sm = O.smooth_k_mean(kh) if smooth else False      # original token order (R28)
         if perm is not None:
             qh, kh, vh = qh[perm], kh[perm], vh[perm]
         o, M, near, cnt, quant = O.spargeattn_head(qh, kh, vh, tau, theta, lam, causal=causal,
                                                    qblocks=qblocks, sim_mode=sim_mode,
-                                                   quantize=quantize, pv_round=pv_round)
+                                                   quantize=quantize, pv_round=pv_round,
+                                                   smooth=sm)
         if perm is not None:
             inv = np.empty_like(perm)
             inv[perm] = np.arange(perm.size)
