@@ -73,7 +73,9 @@ typedef struct {
   int in_dtype;           /* enum sparge_dtype of Q, K, V, O                 */
   int pv_dtype;           /* enum sparge_pv_dtype                            */
   int sim_mode;           /* enum sparge_sim_mode                           */
-  int smooth_k;           /* 0 only (R14); 1 -> SPARGE_ENOTIMPL              */
+  int smooth_k;           /* 0/1: K smoothing (row f4, R28; INT8 QK only):   *
+                           * K goes through sparge_smooth_k_mean +           *
+                           * sparge_quantize_smooth_k                        */
   int qk_dtype;           /* enum sparge_qk_dtype                           */
 } sparge_shape;
 
@@ -115,13 +117,42 @@ int hilbert_permute(int T, int H, int W, int text_prefix,
  *   pooled fp64 [B, H, T, d]: mean over the block's valid rows
  *   sim    fp64 [B, H, T]: CosSim of the block per sim_mode     (R1)
  * T = T_m (is_key = 0) or T_n (is_key = 1).
- * Errors: SPARGE_EINVAL (bad shape, NULL pointer, misaligned stride),
- * SPARGE_ENOTIMPL (smooth_k), SPARGE_ECUDA.
+ * Errors: SPARGE_EINVAL (bad shape, NULL pointer, misaligned stride, K of a
+ * smooth_k shape -- that one goes through sparge_quantize_smooth_k),
+ * SPARGE_ECUDA.
  */
 int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_str,
                     int is_key, const int32_t* perm,
                     void* xq, float* delta, double* pooled, double* sim,
                     void* stream);
+
+/*
+ * K smoothing -- scope row f4, the SageAttention "smooth K" step that the
+ * paper's SageAttention2-based kernel inherits (footnote P:L44; reading R28).
+ * K' = K - mu with mu the per-channel token mean of K: S' = S - q.mu is a
+ * per-query-row constant, so softmax, the lambda gate (m_local - m_new) and O
+ * are unchanged in exact arithmetic, and the INT8 blocks of K' lose the
+ * channel offsets.  Stage 1 (pooled, CosSim, the mask) keeps the raw K (R14).
+ *
+ * sparge_smooth_k_workspace: bytes of fp64 chunk sums sparge_smooth_k_mean
+ * needs (B*Hkv*ceil(N/128)*d doubles); 0 on invalid shape.
+ * sparge_smooth_k_mean: mean fp32 [B, Hkv, d] (caller-allocated) =
+ *   fl32( (sum over chunks of 128 tokens, in chunk order, of the sequential
+ *   fp64 sum of the chunk's tokens in index order) / N ), tokens in their
+ *   ORIGINAL order (before any Hilbert permutation).  k as in sparge_quantize
+ *   (is_key = 1).  workspace: >= sparge_smooth_k_workspace, 8-B aligned.
+ * sparge_quantize_smooth_k: sparge_quantize of K (is_key = 1) whose INT8
+ *   path quantises fl32(k - mean[c]) per element (amax and delta of the
+ *   smoothed block); pooled and sim are those of the raw k.
+ * Errors: SPARGE_EINVAL, SPARGE_ENOTIMPL (qk_dtype INPUT: nothing to
+ * smooth), SPARGE_ECUDA.  No synchronisation.
+ */
+size_t sparge_smooth_k_workspace(const sparge_shape* shape);
+int sparge_smooth_k_mean(const sparge_shape* shape, const void* k, sparge_strides k_str,
+                         void* workspace, size_t ws_bytes, float* mean, void* stream);
+int sparge_quantize_smooth_k(const sparge_shape* shape, const void* k, sparge_strides k_str,
+                             const int32_t* perm, const float* mean, void* kq, float* delta,
+                             double* pooled, double* sim, void* stream);
 
 /*
  * sparge_predict_mask -- stage 1 of Algorithm 1, lines 5-6,
@@ -190,8 +221,8 @@ size_t sparge_attn_workspace(const sparge_shape* shape);
  *   workspace/ws_bytes  >= sparge_attn_workspace(shape), 256-byte aligned;
  *            zero-initialised once by the caller (its first word is the
  *            status word, cleared again by sparge_attn_status)
- * Errors: SPARGE_EINVAL, SPARGE_ENOTIMPL (pv_dtype FP8 with qk_dtype INPUT,
- * smooth_k), SPARGE_ECUDA.  A
+ * Errors: SPARGE_EINVAL, SPARGE_ENOTIMPL (pv_dtype FP8 or smooth_k with
+ * qk_dtype INPUT), SPARGE_ECUDA.  A
  * row finishing with l = 0 is recorded in the workspace status word and
  * reported by sparge_attn_status.
  */

@@ -134,8 +134,35 @@ int sparge_quantize(const sparge_shape* shape, const void* x, sparge_strides x_s
   if (!shape_ok(shape) || !x || !xq || !delta || !pooled || !sim) return SPARGE_EINVAL;
   if (!strides_ok(x_str) || !aligned16(x) || !aligned16(xq)) return SPARGE_EINVAL;
   if (is_key != 0 && is_key != 1) return SPARGE_EINVAL;
-  if (shape->smooth_k) return SPARGE_ENOTIMPL;
-  cudaError_t e = launch_quant(*shape, x, x_str, is_key, perm, xq, delta, pooled, sim,
+  // a smoothed K goes through sparge_quantize_smooth_k (it needs the mean)
+  if (shape->smooth_k && is_key) return SPARGE_EINVAL;
+  cudaError_t e = launch_quant(*shape, x, x_str, is_key, perm, xq, delta, pooled, sim, nullptr,
+                               static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
+}
+
+size_t sparge_smooth_k_workspace(const sparge_shape* shape) {
+  if (!shape_ok(shape)) return 0;
+  return smooth_partial_bytes(*shape);
+}
+
+int sparge_smooth_k_mean(const sparge_shape* shape, const void* k, sparge_strides k_str,
+                         void* workspace, size_t ws_bytes, float* mean, void* stream) {
+  if (!shape_ok(shape) || !k || !workspace || !mean) return SPARGE_EINVAL;
+  if (!strides_ok(k_str) || (reinterpret_cast<uintptr_t>(workspace) & 7u)) return SPARGE_EINVAL;
+  if (ws_bytes < smooth_partial_bytes(*shape)) return SPARGE_EINVAL;
+  cudaError_t e = launch_smooth_mean(*shape, k, k_str, static_cast<double*>(workspace), mean,
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
+}
+
+int sparge_quantize_smooth_k(const sparge_shape* shape, const void* k, sparge_strides k_str,
+                             const int32_t* perm, const float* mean, void* kq, float* delta,
+                             double* pooled, double* sim, void* stream) {
+  if (!shape_ok(shape) || !k || !mean || !kq || !delta || !pooled || !sim) return SPARGE_EINVAL;
+  if (!strides_ok(k_str) || !aligned16(k) || !aligned16(kq)) return SPARGE_EINVAL;
+  if (shape->qk_dtype != SPARGE_QK_INT8) return SPARGE_ENOTIMPL;   // nothing to smooth
+  cudaError_t e = launch_quant(*shape, k, k_str, 1, perm, kq, delta, pooled, sim, mean,
                                static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
 }
@@ -194,7 +221,7 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
   if (!(lambda < 0.f)) return SPARGE_EINVAL;   // lambda < 0 or -inf (§3.6)
   const bool pv8 = shape->pv_dtype == SPARGE_PV_FP8_E4M3;
   if (pv8 && shape->qk_dtype != SPARGE_QK_INT8) return SPARGE_ENOTIMPL;   // FP8 PV with INT8 QK only
-  if (shape->smooth_k) return SPARGE_ENOTIMPL;
+  if (shape->smooth_k && shape->qk_dtype != SPARGE_QK_INT8) return SPARGE_ENOTIMPL;
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const sparge_shape& s = *shape;

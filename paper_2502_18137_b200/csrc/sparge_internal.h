@@ -9,9 +9,16 @@
 
 namespace sparge {
 
+// mu: nullptr, or (K only) the smoothing mean [B, Hkv, d] of k_smooth.cu:
+// the INT8 path quantises fl32(x - mu), the statistics use the raw x (R28, R14)
 cudaError_t launch_quant(const sparge_shape& s, const void* x, sparge_strides st, int is_key,
                          const int32_t* perm, void* xq, float* delta, double* pooled,
-                         double* sim, cudaStream_t stream);
+                         double* sim, const float* mu, cudaStream_t stream);
+
+// K smoothing mean (row f4, R28): fixed-order fp64 chunk sums -> fp32 mean
+size_t smooth_partial_bytes(const sparge_shape& s);
+cudaError_t launch_smooth_mean(const sparge_shape& s, const void* k, sparge_strides st,
+                               double* part, float* mean, cudaStream_t stream);
 
 cudaError_t launch_predict(const sparge_shape& s, const double* q_pooled, const double* q_sim,
                            const double* k_pooled, const double* k_sim, float tau, float theta,

@@ -74,11 +74,20 @@ _lib.sparge_l1_sums.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int64, _vp, _vp
 SPARGE_L1_OUT_DOUBLES = 1186
 _lib.sparge_attn_status.restype = ctypes.c_int
 _lib.sparge_attn_status.argtypes = [_vp, _vp]
+_lib.sparge_smooth_k_workspace.restype = ctypes.c_size_t
+_lib.sparge_smooth_k_workspace.argtypes = [ctypes.POINTER(Shape)]
+_lib.sparge_smooth_k_mean.restype = ctypes.c_int
+_lib.sparge_smooth_k_mean.argtypes = [ctypes.POINTER(Shape), _vp, Strides, _vp, ctypes.c_size_t,
+                                      _vp, _vp]
+_lib.sparge_quantize_smooth_k.restype = ctypes.c_int
+_lib.sparge_quantize_smooth_k.argtypes = [ctypes.POINTER(Shape), _vp, Strides, _vp, _vp, _vp,
+                                          _vp, _vp, _vp, _vp]
 
 EXPORTED = ("sparge_strerror", "hilbert_permute", "sparge_quantize", "sparge_predict_mask",
             "sparge_predict_workspace",
             "sparge_attn_workspace", "sparge_attn_fwd", "sparge_attn_fwd_ex",
-            "sparge_attn_status", "sparge_l1_sums")
+            "sparge_attn_status", "sparge_l1_sums", "sparge_smooth_k_workspace",
+            "sparge_smooth_k_mean", "sparge_quantize_smooth_k")
 SPARGE_ATTN_VPREP_ONLY, SPARGE_ATTN_SKIP_VPREP = 1, 2
 
 
@@ -104,10 +113,10 @@ def _strides(t):
 
 
 def make_shape(B, Hq, Hkv, N, d, causal=False, dtype=torch.bfloat16, sim_mode=SPARGE_SIM_COSINE,
-               qk_dtype=SPARGE_QK_INT8, pv_dtype=SPARGE_PV_SAME_AS_INPUT):
+               qk_dtype=SPARGE_QK_INT8, pv_dtype=SPARGE_PV_SAME_AS_INPUT, smooth_k=False):
     return Shape(B, Hq, Hkv, N, d, 128, 64, 4, int(bool(causal)),
-                 SPARGE_FP16 if dtype == torch.float16 else SPARGE_BF16, int(pv_dtype), sim_mode, 0,
-                 int(qk_dtype))
+                 SPARGE_FP16 if dtype == torch.float16 else SPARGE_BF16, int(pv_dtype), sim_mode,
+                 int(bool(smooth_k)), int(qk_dtype))
 
 
 # ------------------------------------------------------------------ C-ABI calls
@@ -125,6 +134,23 @@ def hilbert_permute(T, H, W, text_prefix=0):
 def sparge_quantize(shape, x, is_key, perm, xq, delta, pooled, sim, stream=None):
     _check("sparge_quantize", _lib.sparge_quantize(
         ctypes.byref(shape), _ptr(x), _strides(x), int(is_key), _ptr(perm), _ptr(xq),
+        _ptr(delta), _ptr(pooled), _ptr(sim), _stream(stream)))
+
+
+def sparge_smooth_k_workspace(shape):
+    return int(_lib.sparge_smooth_k_workspace(ctypes.byref(shape)))
+
+
+def sparge_smooth_k_mean(shape, k, workspace, mean, stream=None):
+    """K smoothing mean (row f4, R28) -> mean fp32 [B, Hkv, d]."""
+    _check("sparge_smooth_k_mean", _lib.sparge_smooth_k_mean(
+        ctypes.byref(shape), _ptr(k), _strides(k), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _ptr(mean), _stream(stream)))
+
+
+def sparge_quantize_smooth_k(shape, k, perm, mean, kq, delta, pooled, sim, stream=None):
+    _check("sparge_quantize_smooth_k", _lib.sparge_quantize_smooth_k(
+        ctypes.byref(shape), _ptr(k), _strides(k), _ptr(perm), _ptr(mean), _ptr(kq),
         _ptr(delta), _ptr(pooled), _ptr(sim), _stream(stream)))
 
 
@@ -218,26 +244,36 @@ class Buffers:
         self.workspace = torch.zeros((ws + 255) // 256 * 256, dtype=torch.uint8, **kw)
         pws = sparge_predict_workspace(shape)
         self.pred_workspace = torch.empty((pws + 255) // 256 * 256, dtype=torch.uint8, **kw)
+        if shape.smooth_k:
+            sws = sparge_smooth_k_workspace(shape)
+            self.smooth_workspace = torch.empty((sws + 255) // 256 * 256, dtype=torch.uint8, **kw)
+            self.k_mean = torch.empty(B, Hkv, d, dtype=torch.float32, **kw)
 
 
 def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=None, out=None,
                    sim_mode=SPARGE_SIM_COSINE, stream=None, qk_dtype=SPARGE_QK_INT8,
-                   pv_dtype=SPARGE_PV_SAME_AS_INPUT):
+                   pv_dtype=SPARGE_PV_SAME_AS_INPUT, smooth_k=False):
     """The whole hot path (a1 quantise Q, K -> a2 predict -> a3 attention) on
     device tensors q [B,Hq,N,d], k/v [B,Hkv,N,d] (bf16 or fp16).  perm: optional
     int32 device tensor [N] (Hilbert order); O is returned in original order.
     qk_dtype=SPARGE_QK_INPUT selects the unquantised "SpargeAttn+FA2" kernel;
-    pv_dtype=SPARGE_PV_FP8_E4M3 the FP8 P~V product (row f4).
+    pv_dtype=SPARGE_PV_FP8_E4M3 the FP8 P~V product and smooth_k=True the K
+    smoothing (row f4, R28).
     Returns (O, buffers)."""
     B, Hq, N, d = q.shape
     Hkv = k.shape[1]
-    shape = make_shape(B, Hq, Hkv, N, d, causal, q.dtype, sim_mode, qk_dtype, pv_dtype)
+    shape = make_shape(B, Hq, Hkv, N, d, causal, q.dtype, sim_mode, qk_dtype, pv_dtype, smooth_k)
     if buffers is None:
         buffers = Buffers(shape, device=q.device)
     bf = buffers
     o = torch.empty_like(q) if out is None else out
     sparge_quantize(shape, q, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim, stream)
-    sparge_quantize(shape, k, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim, stream)
+    if smooth_k:
+        sparge_smooth_k_mean(shape, k, bf.smooth_workspace, bf.k_mean, stream)
+        sparge_quantize_smooth_k(shape, k, perm, bf.k_mean, bf.kq, bf.dk, bf.k_pooled, bf.k_sim,
+                                 stream)
+    else:
+        sparge_quantize(shape, k, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim, stream)
     sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, tau, theta,
                         bf.mask, bf.lut, bf.cnt, bf.pred_workspace, stream)
     sparge_attn_fwd(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm, o,

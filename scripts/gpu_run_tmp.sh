@@ -1,5 +1,2 @@
 set -u
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "quantize or hilbert" > gpurun_out/pytest_q.log 2>&1; echo q_rc=$?; tail -2 gpurun_out/pytest_q.log
-for lib in libsparge_lpt.so libsparge.so; do for w in llama31_8b_32k mochi cogvideox_2b; do
-SPARGE_LIB=$lib timeout 300 python bench.py --workload $w --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-dense --no-f1 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('$lib', '$w', {k:round(v,3) for k,v in d['stages_ms'].items()})"
-done; done
+timeout 900 python -m pytest tests/test_gpu_smooth.py -x -q > gpurun_out/pytest_smooth.log 2>&1; echo rc=$?; tail -25 gpurun_out/pytest_smooth.log

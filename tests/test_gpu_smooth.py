@@ -1,0 +1,89 @@
+"""GPU parity of K smoothing (scope row f4, reading R28) through the C ABI
+against the fp64 oracle: the smoothing mean and the smoothed INT8 K bit for
+bit, stage 1 unchanged (R14), O within the parity tolerance."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import bf16_np, oracle_forward, rel_l1
+from paper_2502_18137_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+BUG_L1 = 5e-3
+
+
+def _dev(x):
+    return inputs.to_device(x, torch.bfloat16)
+
+
+def _smooth_case(lib, k, perm=None):
+    B, H, N, d = k.shape
+    shape = lib.make_shape(B, H, H, N, d, smooth_k=True)
+    T = (N + 63) // 64
+    ws = torch.empty(lib.sparge_smooth_k_workspace(shape), dtype=torch.uint8, device="cuda")
+    mean = torch.empty(B, H, d, dtype=torch.float32, device="cuda")
+    kq = torch.empty(B, H, N, d, dtype=torch.int8, device="cuda")
+    dk = torch.empty(B, H, T, dtype=torch.float32, device="cuda")
+    po = torch.empty(B, H, T, d, dtype=torch.float64, device="cuda")
+    si = torch.empty(B, H, T, dtype=torch.float64, device="cuda")
+    lib.sparge_smooth_k_mean(shape, k, ws, mean)
+    lib.sparge_quantize_smooth_k(shape, k, perm, mean, kq, dk, po, si)
+    torch.cuda.synchronize()
+    return mean.cpu().numpy(), kq.cpu().numpy(), dk.cpu().numpy(), po.cpu().numpy(), si.cpu().numpy()
+
+
+@pytest.mark.parametrize("N,d", [(77, 64), (1000, 128), (4099, 128)])
+def test_mean_and_smoothed_int8_bit_exact(lib, N, d):
+    rng = np.random.default_rng(N + d)
+    x = inputs.gaussian(N, 2, 2, N, d, scale=1.5) + 4.0 * rng.standard_normal(d)[None, None, None]
+    k = _dev(x)
+    mean, kq, dk, po, si = _smooth_case(lib, k)
+    ks = bf16_np(k)
+    for b in range(2):
+        for h in range(2):
+            mu = O.smooth_k_mean(ks[b, h])
+            assert np.array_equal(mean[b, h], mu)
+            q_ref, d_ref = O.quantize_blocks(O.smooth_k(ks[b, h], mu), 64)
+            assert np.array_equal(kq[b, h], q_ref)
+            assert np.array_equal(dk[b, h], d_ref)
+            # stage-1 statistics are those of the raw K (R14)
+            np.testing.assert_allclose(po[b, h], O.block_mean(ks[b, h], 64), rtol=0, atol=1e-13)
+            np.testing.assert_allclose(si[b, h], O.block_sims(ks[b, h], 64), rtol=1e-12, atol=1e-13)
+
+
+def test_smoothed_int8_with_permutation_and_strides(lib):
+    N, d = 1500, 128
+    x = inputs.gaussian(7, 1, 3, N, d) + 3.0
+    k = _dev(x)[:, :, :, :]                                    # [1, 3, N, d]
+    k_strided = torch.empty(1, 3, N, 2 * d, dtype=torch.bfloat16, device="cuda")[..., :d]
+    k_strided.copy_(k)
+    perm = np.random.default_rng(1).permutation(N).astype(np.int32)
+    mean, kq, dk, _, _ = _smooth_case(lib, k_strided, torch.from_numpy(perm).cuda())
+    ks = bf16_np(k)[0]
+    for h in range(3):
+        mu = O.smooth_k_mean(ks[h])                           # original token order (R28)
+        assert np.array_equal(mean[0, h], mu)
+        q_ref, d_ref = O.quantize_blocks(O.smooth_k(ks[h][perm], mu), 64)
+        assert np.array_equal(kq[0, h], q_ref) and np.array_equal(dk[0, h], d_ref)
+
+
+@pytest.mark.parametrize("N,Hq,Hkv,causal", [(1000, 4, 2, True), (1536, 2, 2, False)])
+def test_pipeline_with_smoothing(lib, N, Hq, Hkv, causal):
+    qn, kn, vn = inputs.llm_local(N + 5, N, d=128, Hq=Hq, Hkv=Hkv, gamma=1.5)
+    kn = kn + 2.0 * np.random.default_rng(N).standard_normal(128)      # channel offsets
+    q, k, v = _dev(qn), _dev(kn), _dev(vn)
+    o_s, bf_s = lib.sparge_forward(q, k, v, 0.9, 0.5, -5.0, causal=causal, smooth_k=True)
+    o_p, bf_p = lib.sparge_forward(q, k, v, 0.9, 0.5, -5.0, causal=causal)
+    lib.sparge_attn_status(bf_s.workspace)
+    torch.cuda.synchronize()
+    # stage 1 reads the raw K: identical masks (R14)
+    assert torch.equal(bf_s.mask, bf_p.mask)
+    ref = oracle_forward(bf16_np(q)[0], bf16_np(k)[0], bf16_np(v)[0], 0.9, 0.5, -5.0,
+                         causal=causal, group=Hq // Hkv, smooth=True)
+    og = bf16_np(o_s)[0]
+    for h in range(Hq):
+        err = rel_l1(og[h], ref[h]["o"])
+        assert err < BUG_L1, (h, err)
