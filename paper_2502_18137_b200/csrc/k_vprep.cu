@@ -25,30 +25,44 @@ k_vprep(const uint16_t* __restrict__ v, int64_t sb, int64_t sh, int64_t sn,
   const int jb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x;
   const uint16_t* vbh = v + b * sb + h * sh;
-  // load 64 rows x D (16 B per thread per step), gathered through perm
+  // load 64 rows x D (16 B per thread per step), gathered through perm; the
+  // source rows are looked up first so their loads are all in flight at once
   constexpr int CPR = D / 8;
-  for (int e = tid; e < BK * CPR; e += 256) {
-    const int r = e / CPR, c8 = e % CPR;
-    const int row = jb * BK + r;
-    uint4 val = make_uint4(0, 0, 0, 0);
-    if (row < N) {
-      const int src = perm ? __ldg(perm + row) : row;
-      val = __ldg(reinterpret_cast<const uint4*>(vbh + static_cast<int64_t>(src) * sn + c8 * 8));
-    }
-    *reinterpret_cast<uint4*>(&tile[r][c8 * 8]) = val;
+  constexpr int NL = BK * CPR / 256;
+  int src[NL];
+#pragma unroll
+  for (int q = 0; q < NL; ++q) {
+    const int row = jb * BK + (tid + q * 256) / CPR;
+    src[q] = row < N ? (perm ? __ldg(perm + row) : row) : -1;
+  }
+  uint4 val[NL];
+#pragma unroll
+  for (int q = 0; q < NL; ++q) {
+    const int c8 = (tid + q * 256) % CPR;
+    val[q] = src[q] >= 0
+                 ? __ldg(reinterpret_cast<const uint4*>(vbh + static_cast<int64_t>(src[q]) * sn + c8 * 8))
+                 : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int q = 0; q < NL; ++q) {
+    const int e = tid + q * 256;
+    *reinterpret_cast<uint4*>(&tile[e / CPR][(e % CPR) * 8]) = val[q];
   }
   __syncthreads();
-  // write D rows x 64 keys: 8 keys (16 B) per thread per step
+  // write D rows x 64 keys: thread (c, k16) packs 16 keys (32 B); lanes run
+  // over consecutive c, so the column reads of the tile are conflict-free
   uint16_t* out = vt + ((static_cast<int64_t>(b) * Hkv + h) * D) * n_pad + jb * BK;
-  for (int e = tid; e < D * (BK / 8); e += 256) {
-    const int c = e / (BK / 8), k8 = e % (BK / 8);
-    uint32_t w[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      w[q] = static_cast<uint32_t>(tile[k8 * 8 + 2 * q][c]) |
-             (static_cast<uint32_t>(tile[k8 * 8 + 2 * q + 1][c]) << 16);
-    *reinterpret_cast<uint4*>(out + static_cast<int64_t>(c) * n_pad + k8 * 8) =
-        make_uint4(w[0], w[1], w[2], w[3]);
+  for (int e = tid; e < D * (BK / 16); e += 256) {
+    const int c = e % D, k16 = e / D;
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      w[q] = static_cast<uint32_t>(tile[k16 * 16 + 2 * q][c]) |
+             (static_cast<uint32_t>(tile[k16 * 16 + 2 * q + 1][c]) << 16);
+    uint4* o4 = reinterpret_cast<uint4*>(out + static_cast<int64_t>(c) * n_pad + k16 * 16);
+    o4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    o4[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
 
