@@ -16,10 +16,11 @@
 //               blocks per CTA staged in shared memory (rows padded to d+4
 //               doubles: the A/B fragment loads are bank-conflict free), one
 //               8-row strip per warp; written to the workspace.
-// k_topcdf_rows one warp per (head, query block): masks, softmax, a
-//               warp-synchronous branch-free bitonic sort of 64-bit composite
-//               keys in shared memory, a conflict-free warp scan, threshold,
-//               forcing, causal AND + guard, ballot compaction into the LUT.
+// k_topcdf_rows one warp per (head, query block): masks, softmax, the
+//               sort-free binned TopCdf selection (topcdf_binned: fixed-point
+//               integer bin masses, only the boundary bin sorted; the full
+//               bitonic sorts remain behind SPARGE_TOPCDF_BINNED=0), forcing,
+//               causal AND + guard, ballot compaction into the LUT.
 #include <cstdint>
 #include <cfloat>
 
@@ -154,6 +155,151 @@ __device__ __forceinline__ void sort_desc(uint64_t* key, int lane) {
   }
 }
 
+// Warp-synchronous bitonic sort, descending, of n (a power of two) 64-bit
+// keys in shared memory, runtime n.
+__device__ __forceinline__ void sort_desc_n(uint64_t* key, int n, int lane) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int t = lane; t < n / 2; t += 32) {
+        const int a = t + (t & ~(jj - 1));
+        const int c = a + jj;
+        const uint64_t ka = key[a], kc = key[c];
+        const bool desc_block = (a & k) == 0;
+        const bool sw = desc_block ? (kc > ka) : (ka > kc);
+        key[a] = sw ? kc : ka;
+        key[c] = sw ? ka : kc;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// TopCdf selection without a full sort (v4).  Keys as in the sort path
+// (truncated P^ bits | 2047 - j).  The selected set is a prefix of the
+// descending order, so only the entries of the BOUNDARY bin need ordering:
+//   * P^ is put in fixed point, q_j = floor(p_j * 2^s) with p_max * 2^s in
+//     [2^52, 2^53) (sum < 2^64): integer sums are exact and order-free, so
+//     the result is deterministic and equals the sequential fp64 cumsum up
+//     to ~2^-52 relative (inside the 1e-6 near-threshold band);
+//   * bins by (binade below the max, top 3 mantissa bits): NB = 256 bins in
+//     descending key order, counts and integer mass per bin;
+//   * the boundary bin b* = the first whose cumulative mass exceeds
+//     tau * total; bins before it are selected, bins after it are not, and
+//     the entries of b* are sorted and scanned from the mass above it.
+// tau >= 1 selects everything (c_k <= c_last for every k, R4).  Rank 0 is
+// always selected (guard).  ukey: the keys, entry j at kix(j) (padded when
+// PAD), overwritten: the boundary bin is compacted in place to ukey[0, m)
+// and sorted there; bins: scratch of NB counts + NB sums; flag: [T_n].
+constexpr int kNB = 256;
+__device__ __forceinline__ int bin_of(uint64_t key, int emax) {
+  const int e = static_cast<int>(key >> 52) & 0x7FF;
+  const int db = emax - e;
+  if (db >= kNB / 8) return kNB - 1;
+  return db * 8 + (7 - static_cast<int>((key >> 49) & 7u));
+}
+template <bool PAD>
+__device__ void topcdf_binned(uint64_t* ukey, unsigned int* bcnt, unsigned long long* bsum,
+                              uint8_t* flag, int T_n, double tau, int lane) {
+  auto kix = [](int j) { return PAD ? j + (j >> 5) : j; };
+  uint64_t* list = ukey;
+  // max key -> its exponent; fixed-point scale
+  uint64_t kmax = 0;
+  for (int j = lane; j < T_n; j += 32) kmax = max(kmax, ukey[kix(j)]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  const int emax = static_cast<int>(kmax >> 52) & 0x7FF;
+  const int sc = 52 - (emax - 1023);
+  for (int b = lane; b < kNB; b += 32) bsum[b] = 0ull;
+  (void)bcnt;
+  __syncwarp();
+  unsigned long long part = 0;
+  for (int j = lane; j < T_n; j += 32) {
+    const uint64_t k = ukey[kix(j)];
+    const unsigned long long qj = __double2ull_rz(ldexp(__longlong_as_double(k & ~0x7FFull), sc));
+    const int b = bin_of(k, emax);
+    atomicAdd(&bsum[b], qj);
+    part += qj;
+  }
+  const unsigned long long total = warp_sum_u64(part);
+  __syncwarp();
+  const double thr = (tau >= 1.0) ? INFINITY : tau * static_cast<double>(total);
+  // boundary bin: lane-parallel prefix over the NB bins (8 per lane, in order)
+  unsigned long long lsum = 0;
+#pragma unroll
+  for (int u = 0; u < kNB / 32; ++u) lsum += bsum[lane * (kNB / 32) + u];
+  unsigned long long incl = lsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  unsigned long long above = incl - lsum;   // mass of bins before this lane's first
+  int bstar = kNB;
+  unsigned long long a_star = 0;
+#pragma unroll
+  for (int u = 0; u < kNB / 32; ++u) {
+    const int b = lane * (kNB / 32) + u;
+    const unsigned long long nxt = above + bsum[b];
+    if (bstar == kNB && static_cast<double>(nxt) > thr) { bstar = b; a_star = above; }
+    above = nxt;
+  }
+  // the first such bin over the warp
+  int bmin = bstar;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+  const unsigned int owner = __ballot_sync(0xffffffffu, bstar == bmin && bmin < kNB);
+  if (bmin < kNB) a_star = __shfl_sync(0xffffffffu, a_star, __ffs(owner) - 1);
+  // flags outside the boundary bin; compact the boundary bin's keys in place
+  // (write index m + rank <= j0 + lane <= kix(j0 + lane): never ahead of an
+  // unread key, and the reads of a chunk precede its writes)
+  int m = 0;
+  for (int j0 = 0; j0 < T_n; j0 += 32) {
+    const int j = j0 + lane;
+    const uint64_t k = (j < T_n) ? ukey[kix(j)] : 0ull;
+    const int b = (j < T_n) ? bin_of(k, emax) : kNB;
+    const bool inb = (j < T_n) && (b == bmin);
+    if (j < T_n) flag[j] = (b < bmin) ? 1 : 0;
+    const unsigned int bal = __ballot_sync(0xffffffffu, inb);
+    __syncwarp();
+    if (inb) list[m + __popc(bal & ((1u << lane) - 1u))] = k;
+    m += __popc(bal);
+    __syncwarp();
+  }
+  if (bmin < kNB) {
+    int n2 = 2;
+    while (n2 < m) n2 <<= 1;
+    for (int t = m + lane; t < n2; t += 32) list[t] = 0ull;
+    __syncwarp();
+    sort_desc_n(list, n2, lane);
+    // sequential scan of the bin (in chunks of 32, integer prefix sums)
+    unsigned long long carry = a_star;
+    for (int t0 = 0; t0 < m; t0 += 32) {
+      const int t = t0 + lane;
+      const uint64_t k = (t < m) ? list[t] : 0ull;
+      unsigned long long qv =
+          (t < m) ? __double2ull_rz(ldexp(__longlong_as_double(k & ~0x7FFull), sc)) : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, qv, o);
+        if (lane >= o) qv += y;
+      }
+      const unsigned long long c = carry + qv;
+      if (t < m) flag[2047 - static_cast<int>(k & 0x7FFull)] = (static_cast<double>(c) <= thr) ? 1 : 0;
+      carry = __shfl_sync(0xffffffffu, c, 31);
+    }
+  }
+  __syncwarp();
+  // guard: the top entry
+  if (lane == 0) flag[2047 - static_cast<int>(kmax & 0x7FFull)] = 1;
+  __syncwarp();
+}
+
 // Register bitonic sort, descending, of SORTN = 32*R 64-bit keys held
 // lane-major (rank i = lane*R + r): stages with partner distance jj < R are
 // compare-exchanges between two registers of one lane, stages with jj >= R
@@ -246,7 +392,12 @@ __device__ __forceinline__ void topcdf_reg(uint64_t* ukey, uint8_t* flag, int T_
 }
 
 // RS = SORTN / 32 for the register sort (SORTN <= 1024), 0 = the
-// shared-memory sort (SORTN = 2048).
+// shared-memory sort (SORTN = 2048).  SPARGE_TOPCDF_BINNED (default): the
+// sort-free binned selection above instead of either sort.
+#ifndef SPARGE_TOPCDF_BINNED
+#define SPARGE_TOPCDF_BINNED 1
+#endif
+constexpr bool kBinned = SPARGE_TOPCDF_BINNED != 0;
 #ifndef SPARGE_TOPCDF_MINB32
 #define SPARGE_TOPCDF_MINB32 3
 #endif
@@ -264,6 +415,10 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   uint64_t* ukey = reinterpret_cast<uint64_t*>(smem) + wid * kstride;
   double* key = reinterpret_cast<double*>(ukey);
   uint8_t* flag = smem + static_cast<size_t>(kRowWarps) * kstride * 8 + wid * sortn;
+  // binned selection scratch: NB bin sums + NB bin counts per warp
+  unsigned long long* bsum = reinterpret_cast<unsigned long long*>(
+      smem + static_cast<size_t>(kRowWarps) * (kstride * 8 + sortn)) + wid * kNB;
+  unsigned int* bcnt = reinterpret_cast<unsigned int*>(bsum + (kRowWarps - wid) * kNB) + wid * kNB;
 
   const int i = row % T_m, bhq = row / T_m;
   const int hq = bhq % Hq, b = bhq / Hq;
@@ -300,7 +455,15 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
     // truncation of P^ -- far inside the 1e-6 near-threshold band of the
     // parity criterion; the cumulative sum uses the truncated values.
     // Padding keys are 0 and sort last (a real entry has key >= 2047 - j > 0).
-    if (RS > 0) {
+    if (kBinned) {
+      for (int j = lane; j < T_n; j += 32) {
+        const int pj = kix(j);
+        ukey[pj] = (static_cast<uint64_t>(__double_as_longlong(key[pj] / total)) & ~0x7FFull) |
+                   static_cast<uint64_t>(2047 - j);
+      }
+      __syncwarp();
+      topcdf_binned<padded>(ukey, bcnt, bsum, flag, T_n, tau, lane);
+    } else if (RS > 0) {
       // register sort: composite keys in place at the padded positions,
       // read back lane-major
       for (int j = lane; j < sortn; j += 32) {
@@ -390,7 +553,7 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
                                                         shat);
   int sortn = 32;
   while (sortn < T_n) sortn <<= 1;
-  const size_t smem_r = static_cast<size_t>(kRowWarps) * ((sortn + sortn / 32) * 8 + sortn);
+  const size_t smem_r = static_cast<size_t>(kRowWarps) * ((sortn + sortn / 32) * 8 + sortn + kNB * 12);
   const int rows = s.B * s.Hq * T_m;
   auto run = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
