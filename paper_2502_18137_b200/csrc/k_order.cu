@@ -88,20 +88,20 @@ k_order_head(const int32_t* __restrict__ cnt, int n, int tn, int per_group, int 
   __syncthreads();
   for (int x = tid; x < n; x += kThreads) atomicAdd(&h[cnt_of(cnt, x, tn)], 1);
   __syncthreads();
-  // cut = the largest value c such that #items with cnt > c >= ... : scan
-  // from the top until n_long_max items are covered (whole buckets only)
-  if (tid == 0) {
-    int acc = 0, cut = tn;
-    for (int b = tn; b >= 0; --b) {
-      if (acc + h[b] > n_long_max) break;
-      acc += h[b];
-      cut = b - 1;
-    }
-    s_cut = cut;
-    meta[0] = cut;
-  }
+  // cut: the long items are the whole top buckets b > cut holding at most
+  // n_long_max items.  #items with cnt >= b is non-increasing in b, so
+  // cut = (the smallest b with #(cnt >= b) <= n_long_max) - 1, found in
+  // parallel from a descending exclusive scan of a copy of the histogram
+  int* ge = gcount + n_groups;            // tn + 1 scan slots
+  for (int b = tid; b <= tn; b += kThreads) ge[b] = h[b];
+  if (tid == 0) s_cut = tn + 1;
   __syncthreads();
-  const int cut = s_cut;
+  scan_desc(ge, tn, warp_sum);           // ge[b] = #(cnt > b)
+  for (int b = tid; b <= tn; b += kThreads)
+    if (ge[b] + h[b] <= n_long_max) atomicMin(&s_cut, b);
+  __syncthreads();
+  const int cut = s_cut - 1;
+  if (tid == 0) meta[0] = cut;
   for (int x = tid; x < n; x += kThreads)
     if (cnt_of(cnt, x, tn) <= cut) atomicAdd(&gcount[x / per_group], 1);
   for (int b = tid; b <= cut; b += kThreads) h[b] = 0;   // only long buckets stay
@@ -155,7 +155,7 @@ cudaError_t launch_order(const int32_t* cnt, int n, int tn, int per_group, int n
                          int32_t* order, int32_t* meta, cudaStream_t stream) {
   per_group = max(1, min(per_group, n));
   const int n_groups = (n + per_group - 1) / per_group;
-  const int smem_head = (tn + 1 + n_groups) * static_cast<int>(sizeof(int));
+  const int smem_head = (2 * (tn + 1) + n_groups) * static_cast<int>(sizeof(int));
   const int smem_groups = (tn + 1) * static_cast<int>(sizeof(int));
   if (smem_head > 200 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_order_head, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_head);
