@@ -146,6 +146,9 @@ constexpr bool kBiasMma = SPARGE_BIAS_MMA != 0;
 constexpr uint16_t kBf16One = 0x3F80;        // bf16 1.0
 constexpr uint16_t kBf16MagicPart = 0x4940;  // bf16 786432 = 1.5*2^19 (x 16 = 1.5*2^23)
 
+#ifndef SPARGE_NSB64
+#define SPARGE_NSB64 2
+#endif
 template <int D, bool QK16, bool PV8 = false>
 struct Smem {
   static constexpr int EB = QK16 ? 2 : 1;       // bytes per Q/K element
@@ -164,7 +167,12 @@ struct Smem {
   static constexpr int OFF_CA = OFF_V + VST * V_BYTES;
   static constexpr int OFF_CB = OFF_CA + CA_BYTES;
   static constexpr int OFF_BAR = OFF_CB + CB_BYTES;
-  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 3;
+  // S ring depth: d = 128 fits two 64-column S buffers next to O in 256
+  // TMEM columns (2*64 + 128); d = 64 would fit three (3*64 + 64), but the
+  // third buffer measured no faster on CogVideoX (1.067 vs 1.058 ms: the
+  // d = 64 kernel is softmax-bound), so SPARGE_NSB64 = 3 is an option only
+  static constexpr int NSB = SPARGE_NSB64 > 0 && D == 64 ? SPARGE_NSB64 : 2;
+  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 3 * 3;
   static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;    // [0] TMEM base, [1..8] pv flags
   static constexpr int TOTAL = OFF_MISC + 64;
   static constexpr int GROUP = (TOTAL + 1023) / 1024 * 1024;
@@ -378,10 +386,10 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         mbar_init(bg + 1 + 2 * KST + VST + s, 1);
       }
       uint64_t* sf = bg + 1 + 2 * KST + 2 * VST;
-      for (int s = 0; s < 2; ++s) {
-        mbar_init(sf + s, 1);            // s_full
-        mbar_init(sf + 2 + s, NSOFT);    // p_full
-        mbar_init(sf + 4 + s, 1);        // o_done
+      for (int s = 0; s < L::NSB; ++s) {
+        mbar_init(sf + s, 1);               // s_full
+        mbar_init(sf + L::NSB + s, NSOFT);  // p_full
+        mbar_init(sf + 2 * L::NSB + s, 1);  // o_tail
       }
     }
     fence_mbar_init();
@@ -422,16 +430,20 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   uint64_t* k_empty = k_full + KST;
   uint64_t* v_full = k_empty + KST;
   uint64_t* v_empty = v_full + VST;
-  uint64_t* s_full = v_empty + VST;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* o_done = p_full + 2;
-  uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC) + 1;       // [2][4]
+  constexpr int NSB = L::NSB;
+  uint64_t* s_full = v_empty + VST;          // [NSB]
+  uint64_t* p_full = s_full + NSB;           // [NSB]
+  uint64_t* o_tail = p_full + NSB;           // [NSB], each completes once
+  uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC) + 1;       // [NSB][4]
   int i = 0, i_other = 0;
   const int n_tiles = tile_of(g, i);
   const int n_other = (NG == 2) ? tile_of(g ^ 1, i_other) : 0;
   const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + min(i, p.T_m - 1);
   const int32_t* lut_row = p.lut + row_id * p.T_n;
-  const uint32_t tS0 = tmem_base + g * 256, tO = tS0 + 128;
+  const uint32_t tS0 = tmem_base + g * 256, tO = tS0 + NSB * BK;
+  // P~V(u) of the last NSB tiles, u >= n - NSB, completes o_tail[u - max(0,
+  // n - NSB)] -- a barrier used once, so its parity-0 wait is unambiguous
+  auto wait_tail = [&](int u) { mbar_wait(o_tail + (u - max(0, n_tiles - NSB)), 0); };
 
   if (warp >= R::LOAD0 && warp < R::MMA0) {
     // ============================ TMA producer ============================
@@ -489,8 +501,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       mbar_wait(q_full, 0);
       tc_fence_after();
       auto do_pv = [&](int u) {
-        const int pb = u & 1, vs = u % VST;
-        mbar_wait(p_full + pb, (u >> 1) & 1);
+        const int pb = u % NSB, vs = u % VST;
+        mbar_wait(p_full + pb, (u / NSB) & 1);
         mbar_wait(v_full + vs, (u / VST) & 1);
         tc_fence_after();
         const bool any = (pv_flag[pb * 4 + 0] | pv_flag[pb * 4 + 1] |
@@ -515,19 +527,21 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           ++issued;
         }
         tc_commit(v_empty + vs);
-        // o_done completes after P~V(n-2) and P~V(n-1) only: the softmax's
-        // rare O rescale at tile t <= n-2 waits on s_full(t+1) instead (QK(t+1)
-        // is issued after P~V(t-1)), the one at tile n-1 and the epilogue on
-        // o_done -- one tcgen05.commit (~44 issue cycles) less per tile
-        if (u + 2 >= n_tiles) tc_commit(o_done);
+        // only the last NSB P~V signal completion (o_tail): the softmax's
+        // rare O rescale at tile t waits on s_full(t+NSB-1) instead (QK(t+NSB-1)
+        // is issued after P~V(t-1)) while that tile exists, else on o_tail, as
+        // does the epilogue -- one tcgen05.commit (~44 issue cycles) less per
+        // tile
+        if (u + NSB >= n_tiles) tc_commit(o_tail + (u - max(0, n_tiles - NSB)));
       };
-      for (int t = 0; t < n_tiles; ++t) {
-        const int ks = t % KST, sb = t & 1;
+      // QK(t) into S[t % NSB]: issued right after P~V(t - NSB), the previous
+      // reader of that buffer (tcgen05.mma from one thread execute in issue
+      // order; the softmax warps finished reading S(t-NSB) before they
+      // arrived on its p_full).  Order: QK(0..NSB-2), then per t: QK(t+NSB-1),
+      // P~V(t) -- the S ring runs NSB-1 tiles ahead of the P~V.
+      auto issue_qk = [&](int t) {
+        const int ks = t % KST, sb = t % NSB;
         mbar_wait(k_full + ks, (t / KST) & 1);
-        // S[sb] holds P~(t-2), read by P~V(t-2), which this thread issued
-        // before this QK(t): tcgen05.mma from one thread execute in issue
-        // order, so no completion wait is needed (the softmax warps finished
-        // reading S(t-2) before they arrived on p_full(t-2)).
         tc_fence_after();
         const uint64_t dK = umma_desc_kmajor(smem_u32(sK + ks * L::K_BYTES), L::ROW_BYTES_QK);
         if (QK16) {
@@ -546,9 +560,12 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         }
         tc_commit(s_full + sb);
         tc_commit(k_empty + ks);
-        if (t > 0) do_pv(t - 1);
+      };
+      for (int t = 0; t < NSB - 1 && t < n_tiles; ++t) issue_qk(t);
+      for (int t = 0; t < n_tiles; ++t) {
+        if (t + NSB - 1 < n_tiles) issue_qk(t + NSB - 1);
+        do_pv(t);
       }
-      do_pv(n_tiles - 1);
       if (p.counters) atomicAdd(p.counters + bhq * 3 + 2, issued);
     }
   } else {
@@ -601,7 +618,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     if (threadIdx.x == 0) { CTA_REC(1, gtimer()); CTA_REC(5, n_tiles); }
 #endif
     for (int t = 0; t < n_tiles; ++t) {
-      const int sb = t & 1;
+      const int sb = t % NSB;
       const uint32_t tS = tS0 + sb * BK + lane_base;
       int32_t a[BK];
       uint32_t pw[BK / 2];
@@ -620,7 +637,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         c = __shfl_sync(0xffffffffu, cc_, tl);
 
         PT_MARK(0);
-        mbar_wait(s_full + sb, (t >> 1) & 1);
+        mbar_wait(s_full + sb, (t / NSB) & 1);
 #ifdef SPARGE_ABL_NOSOFT   // timing ablation only (wrong results): MMA/sync pipeline floor
         tc_fence_after();
         tc_fence_before();
@@ -740,8 +757,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           // O rows of this warp hold P~V of earlier tiles: wait for the last
           // issued P~V, then rescale in TMEM (before p_full(t) releases P~V(t)).
           if (t >= 1) {
-            if (t + 1 < n_tiles) mbar_wait(s_full + ((t + 1) & 1), ((t + 1) >> 1) & 1);
-            else mbar_wait(o_done, 0);     // completion 0 = P~V(n-2)
+            const int tq = t + NSB - 1;
+            if (tq < n_tiles) mbar_wait(s_full + tq % NSB, (tq / NSB) & 1);
+            else wait_tail(t - 1);   // P~V(t-1)
           }
           tc_fence_after();
 #pragma unroll
@@ -789,7 +807,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
     if (threadIdx.x == 0) CTA_REC(2, gtimer());
 #endif
     // ---- epilogue: O_i = O / l (line 19), scattered back through perm ----
-    if (n_tiles > 0) mbar_wait(o_done, n_tiles >= 2 ? 1 : 0);   // P~V(n-1)
+    if (n_tiles > 0) wait_tail(n_tiles - 1);   // P~V(n-1)
     tc_fence_after();
     if (row_valid && !(l > 0.f)) atomicOr(p.status, 1u);
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
