@@ -224,3 +224,42 @@ def test_launch_order_is_longest_first_permutation(lib, N, Hq, Hkv, causal):
     assert c[0] == cnt.max()
     runs = 1 + int(np.sum(np.diff(c) > 0))
     assert runs <= 1 + Hkv, runs
+
+
+@pytest.mark.parametrize("d,is_key", [(128, 0), (64, 1)])
+def test_quantize_fp16_bit_exact(lib, d, is_key):
+    """fp16 inputs: the same R11 arithmetic on the exactly widened values."""
+    N = 1000
+    x = _dev(inputs.gaussian(N + d, 1, 2, N, d, scale=3.0), torch.float16)
+    shape = lib.make_shape(1, 2, 2 if is_key else 1, N, d, False, torch.float16)
+    bs = 64 if is_key else 128
+    T = math.ceil(N / bs)
+    xq = torch.empty(1, 2, N, d, dtype=torch.int8, device="cuda")
+    dl = torch.empty(1, 2, T, dtype=torch.float32, device="cuda")
+    po = torch.empty(1, 2, T, d, dtype=torch.float64, device="cuda")
+    si = torch.empty(1, 2, T, dtype=torch.float64, device="cuda")
+    lib.sparge_quantize(shape, x, is_key, None, xq, dl, po, si)
+    torch.cuda.synchronize()
+    xs = bf16_np(x)[0]
+    for h in range(2):
+        q_ref, d_ref = O.quantize_blocks(xs[h], bs)
+        assert np.array_equal(xq.cpu().numpy()[0, h], q_ref)
+        assert np.array_equal(dl.cpu().numpy()[0, h], d_ref)
+        np.testing.assert_allclose(po.cpu().numpy()[0, h], O.block_mean(xs[h], bs), rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("N,d,Hq,Hkv,causal", [(1000, 128, 4, 2, True), (900, 64, 2, 2, False)])
+def test_pipeline_fp16(lib, N, d, Hq, Hkv, causal):
+    """fp16 Q/K/V: the INT8 kernel with fp16 P~ (lazy-rescale threshold 15,
+    R22) against the oracle with unrounded P~ (the fp16 rounding of P~ and O
+    is ~5e-4 relative, inside the 5e-3 bug threshold)."""
+    qn, kn, vn = inputs.llm_local(N + 3, N, d=d, Hq=Hq, Hkv=Hkv, gamma=1.5)
+    q, k, v = (_dev(a, torch.float16) for a in (qn, kn, vn))
+    o, bf = _run(lib, q, k, v, 0.9, 0.5, -5.0, causal)
+    ref = oracle_forward(bf16_np(q)[0], bf16_np(k)[0], bf16_np(v)[0], 0.9, 0.5, -5.0,
+                         causal=causal, group=Hq // Hkv, pv_round=None)
+    gm = bf.mask.cpu().numpy()[0]
+    og = bf16_np(o)[0]
+    for h in range(Hq):
+        _check_masks(gm[h], ref[h], f"head {h}")
+        assert rel_l1(og[h], ref[h]["o"]) < BUG_L1
