@@ -209,7 +209,12 @@ def run_ours(args):
              shape=shape, bf=bf):
         if ev: ev[0].record()
         sparge.sparge_quantize(shape, q_, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim)
-        sparge.sparge_quantize(shape, k_, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim)
+        if shape.smooth_k:        # row f4 K smoothing: mean, then INT8 of K - mean
+            sparge.sparge_smooth_k_mean(shape, k_, bf.smooth_workspace, bf.k_mean)
+            sparge.sparge_quantize_smooth_k(shape, k_, perm, bf.k_mean, bf.kq, bf.dk, bf.k_pooled,
+                                            bf.k_sim)
+        else:
+            sparge.sparge_quantize(shape, k_, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim)
         if ev: ev[1].record()
         sparge.sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, t, th,
                                    bf.mask, bf.lut, bf.cnt, bf.pred_workspace)
@@ -338,9 +343,9 @@ def run_ours(args):
     # ---- NEXT rows on the same inputs and hyper-parameters: f1 = the
     # unquantised "SpargeAttn+FA2" kernel (bf16 QK^T, Fig. 7); f4 =
     # FP8 E4M3 P~V on INT8 QK^T (SageAttention2-style, footnote P:L44) ----
-    def variant(key, qk_dtype, pv_dtype, peak_tflops):
+    def variant(key, qk_dtype, pv_dtype, peak_tflops, smooth_k=False):
         shape_v = sparge.make_shape(1, Hq, Hkv, N, d, cfg["causal"], q.dtype,
-                                    qk_dtype=qk_dtype, pv_dtype=pv_dtype)
+                                    qk_dtype=qk_dtype, pv_dtype=pv_dtype, smooth_k=smooth_k)
         bv = sparge.Buffers(shape_v, device=dev)
         Kf = min(K, 10)
         evf = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(Kf)]
@@ -376,6 +381,9 @@ def run_ours(args):
         variant("f1_fa2_bf16qk", sparge.SPARGE_QK_INPUT, sparge.SPARGE_PV_SAME_AS_INPUT, bf16_peak)
         # INT8 QK + FP8 PV: both at 2x the bf16 rate (nominal 4.5 vs 2.25 POPS)
         variant("f4_fp8_pv", sparge.SPARGE_QK_INT8, sparge.SPARGE_PV_FP8_E4M3, i8_peak)
+        # K smoothing (row f4, R28) on the default INT8 QK / 16-bit PV path
+        variant("f4_smooth_k", sparge.SPARGE_QK_INT8, sparge.SPARGE_PV_SAME_AS_INPUT, mix_peak,
+                smooth_k=True)
 
     # ---- e2e through the public API with host buffers ----
     if not args.no_e2e:
