@@ -263,3 +263,24 @@ def test_pipeline_fp16(lib, N, d, Hq, Hkv, causal):
     for h in range(Hq):
         _check_masks(gm[h], ref[h], f"head {h}")
         assert rel_l1(og[h], ref[h]["o"]) < BUG_L1
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_pipeline_batch2(lib, causal):
+    """B = 2: every kernel indexes (batch, head) work items -- the launch order
+    mixes both batch elements; each must match its own oracle run."""
+    N, d, Hq, Hkv = 1000, 128, 4, 2
+    qa, ka, va = inputs.llm_local(11, N, d=d, Hq=Hq, Hkv=Hkv, gamma=1.5)
+    qb, kb, vb = inputs.llm_local(12, N, d=d, Hq=Hq, Hkv=Hkv, gamma=1.5)
+    q, k, v = (_dev(np.concatenate([a, b_], axis=0)) for a, b_ in ((qa, qb), (ka, kb), (va, vb)))
+    o, bf = _run(lib, q, k, v, 0.9, 0.5, -5.0, causal)
+    gm = bf.mask.cpu().numpy()
+    og = bf16_np(o)
+    cnt = bf.counters.cpu().numpy()
+    for b in range(2):
+        ref = oracle_forward(bf16_np(q)[b], bf16_np(k)[b], bf16_np(v)[b], 0.9, 0.5, -5.0,
+                             causal=causal, group=Hq // Hkv)
+        for h in range(Hq):
+            _check_masks(gm[b, h], ref[h], f"batch {b} head {h}")
+            assert rel_l1(og[b, h], ref[h]["o"]) < BUG_L1
+            assert cnt[b, h, 0] == ref[h]["cnt"]["qk"]
