@@ -11,36 +11,34 @@
 //        O[I_w] = e^{m - m_new} O[I_w] + P~[I_w] V_j  line 16
 //   O_i = O / l                                       line 19
 //
-// sm_100a design.  A query-tile GROUP = 4 softmax warps + 1 TMA producer
-// warp + 1 MMA warp, 256 TMEM columns (S0 | S1, 64 cols each | O, d cols) and
-// its own K^ / V^T smem rings.  Default: one group per CTA, two CTAs per SM
-// (SPARGE_PAIR=1, an experiment: two groups per CTA, 384 threads, 512 TMEM
-// columns, one CTA per SM).
+// sm_100a design.  A CTA = 4 softmax warps + 1 TMA producer warp + 1 MMA
+// warp, 256 TMEM columns (S0 | S1, 64 cols each | O, d cols), two CTAs per
+// SM; the grid is the launch order of k_order (longest work items first).
 //   producer  Q^ once, then K^_j (4-stage ring) and V^T_j (3-stage ring) for
 //             every kept j; SWIZZLE_128B/64B tiles.
-//   MMA       one thread: tcgen05.mma kind::i8 Q^K^^T -> S[t%2] (kind::f16
-//             for the unquantised f1 kernel), then kind::f16 P~ V -> O with
-//             P~ read from TMEM (TS form).  QK(t) is issued right after
-//             P~V(t-2) (in-order tensor pipe).  The P~V MMA is skipped when
-//             all four row groups vote to skip (their P~ rows are zero
-//             otherwise: exact).
+//   MMA       one thread: per tile a bias MMA (S := fp32 bits of 1.5*2^23),
+//             then tcgen05.mma kind::i8 Q^K^^T accumulating onto it ->
+//             S[t%2] (kind::f16 for the unquantised f1 kernel), then
+//             kind::f16 P~ V -> O with P~ read from TMEM (TS form).  QK(t+1)
+//             is issued right after P~V(t-1) (in-order tensor pipe).  The
+//             P~V MMA is skipped when all four row groups vote to skip
+//             (their P~ rows are zero otherwise: exact).
 //   softmax   thread r owns row r == TMEM lane r; warp w is the gate group
 //             I_w (rows 32w..32w+31).  exp2 domain (lambda compared as
 //             lambda*log2e); the gate max is a warp vote (max_r gap_r >
-//             lambda <=> any_r gap_r > lambda); integer row max; exact
-//             int->fp32 via the 1.5*2^23 magic constant folded into the FFMA
-//             bias (R23); packed f32x2 arithmetic; all exponentials on the
-//             MUFU (SPARGE_POLY_EVERY=k moves 1 pair in k to the FMA pipe,
-//             exp2_poly2: slower since the MUFU is not the bound); P~ (16-bit) written
-//             back into the first 32 columns of its own S buffer; lazy O
-//             rescale (R22: the reference max moves only when the true max
-//             grows by > 16 in log2 units (15 for fp16 P~); O/l is invariant to the reference,
-//             the gate always uses the true running max).  With two groups
-//             the exp bursts of the two warps sharing an SMSP alternate
-//             (named-barrier ping-pong), so the MUFU stays busy while the
-//             other warp does its per-tile bookkeeping (measured: no gain).
-//   (profiles/experiments/k_attn_v3_splitrow_speculative.cu: a variant with
-//   rows split over 8 softmax warps -- correct, but slower at 96 registers.)
+//             lambda <=> any_r gap_r > lambda); integer row max over the
+//             biased fp32 bits; one FFMA per element dequantises and applies
+//             the reference (R23); packed f32x2 arithmetic; all exponentials
+//             on the MUFU (SPARGE_POLY_EVERY=k moves 1 pair in k to the FMA
+//             pipe, exp2_poly2: slower, the MUFU is not the bound); P~
+//             (16-bit) written back into the first 32 columns of its own S
+//             buffer; lazy O rescale (R22: the reference max moves only when
+//             the true max grows by > 16 in log2 units, 15 for fp16 P~; O/l is
+//             invariant to the reference, the gate always uses the true
+//             running max).
+//   (Experiments -- two query tiles per CTA with ping-pong exp bursts, rows
+//   split over 8 softmax warps, 128-key pair iterations, speculative exps --
+//   are in profiles/experiments/ and the git history.)
 #include <cuda.h>
 #include <cstdint>
 #include <climits>
@@ -97,42 +95,16 @@ constexpr float kMagicF = 12582912.0f;
 #endif
 constexpr int kPolyEvery = SPARGE_POLY_EVERY;   // one pair in kPolyEvery uses exp2_poly2 (0: none)
 
-// SPARGE_PAIR=1 (experiment, off): one CTA per SM runs two query tiles
-// (NG = 2 groups, each with its own 4 softmax warps, producer warp, MMA warp,
-// smem rings and 256 TMEM columns), optionally with a ping-pong hand-off of
-// the exp bursts between the two warps that share an SMSP (SPARGE_PINGPONG).
-// Measured on Llama 32K: 4.26 ms with ping-pong, 4.23 ms without, vs 3.88 ms
-// for the default of one tile per CTA and two CTAs per SM -- the MUFU
-// contention between co-resident exp bursts is not what limits the softmax.
-#ifndef SPARGE_PAIR
-#define SPARGE_PAIR 0
-#endif
-constexpr bool kPairs = SPARGE_PAIR != 0;
-#ifndef SPARGE_PINGPONG
-#define SPARGE_PINGPONG 1
-#endif
-constexpr bool kPingPong = SPARGE_PINGPONG != 0;
+// CTA roles: softmax warps 0-3 (one per TMEM lane quadrant), TMA producer
+// warp 4, MMA issuer warp 5.  (Experiments with two query tiles per CTA, a
+// speculative exp pass and timing ablations live in the git history and
+// profiles/experiments/; DESIGN.md §6 has their measurements.)
+constexpr int WARP_LOAD = NSOFT, WARP_MMA = NSOFT + 1;
+constexpr int THREADS = (NSOFT + 2) * 32;
 
-// SPARGE_SPEC (experiment, off: measured slower on Llama/Mochi/CogVideoX):
-// interior tiles compute P~ with the current
-// reference max before the row max is known (see the softmax loop).
-#ifndef SPARGE_SPEC
-#define SPARGE_SPEC 0
-#endif
-constexpr bool kSpec = SPARGE_SPEC != 0 && !kPairs;
-
-template <int NG>
-struct Roles {
-  static constexpr int SOFT = NSOFT * NG;        // softmax warps 4g .. 4g+3
-  static constexpr int LOAD0 = SOFT;             // TMA producer of group g: LOAD0 + g
-  static constexpr int MMA0 = SOFT + NG;         // MMA issuer of group g: MMA0 + g
-  static constexpr int THREADS = (SOFT + 2 * NG) * 32;
-};
-
-// Shared-memory plan of one query-tile group.  QK16 = the unquantised f1
-// kernel (16-bit Q, K tiles stored as d/64 SWIZZLE_128B K-atoms of 128 B
-// rows); with d = 128 its rings shrink to 2 + 2 stages so that two groups
-// still fit on an SM.
+// Shared-memory plan of a CTA.  QK16 = the unquantised f1 kernel (16-bit Q,
+// K tiles stored as d/64 SWIZZLE_128B K-atoms of 128 B rows); with d = 128
+// its rings shrink to 2 + 2 stages so that two CTAs still fit on an SM.
 // SPARGE_BIAS_MMA (INT8 QK): before the kind::i8 MMAs of a tile, one
 // kind::f16 MMA (M128 N64 K16, constant operands 1.0 x 1.5*2^19 summed over
 // K = 16) writes the fp32 value 1.5*2^23 into every S accumulator; the i8
@@ -175,12 +147,12 @@ struct Smem {
   static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 3 * 3;
   static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;    // [0] TMEM base, [1..8] pv flags
   static constexpr int TOTAL = OFF_MISC + 64;
-  static constexpr int GROUP = (TOTAL + 1023) / 1024 * 1024;
+  static constexpr int BYTES = (TOTAL + 1023) / 1024 * 1024;
   // INT8: one K-atom of D bytes per row (128 -> SW128, 64 -> SW64); 16-bit:
   // 128-B atoms, the second (d = 128) BQ*128 / BK*128 bytes after the first
   static constexpr int ROW_BYTES_QK = QK16 ? 128 : D;
   static constexpr int Q_ATOM = BQ * 128, K_ATOM = BK * 128;
-  static_assert(2 * GROUP + 1024 <= 227 * 1024, "two groups must fit one SM");
+  static_assert(2 * (BYTES + 1024) <= 227 * 1024, "two CTAs must fit one SM");
 };
 
 struct AttnParams {
@@ -194,7 +166,7 @@ struct AttnParams {
   unsigned long long* counters;
   unsigned int* status;
   const float* v_scale;   // PV8: per-(b, hkv, channel) dequant scale s_c [B*Hkv, D]
-  const int32_t* order;   // work items (bhq * T_m + i) by descending cnt (k_order, NG = 1)
+  const int32_t* order;   // work items (bhq * T_m + i), the launch order of k_order
   float lam2;         // lambda * log2(e)
   float scale_log2;   // log2(e) / sqrt(d)
   int N, T_m, T_n, Hq, Hkv, group;
@@ -304,11 +276,7 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
     if (!MASKED && kPolyEvery > 0 && ((k >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
       e2 = exp2_poly2(x2);
     else
-#ifdef SPARGE_ABL_NOEXP   // timing ablation only (wrong results): no MUFU
-      e2 = fma2(x2, pk(1e-3f, 1e-3f), pk(1.f, 1.f));
-#else
       e2 = pk(ex2_approx(lo_f(x2)), ex2_approx(hi_f(x2)));
-#endif
     if (MASKED) {
       const float e0 = (a[k] == kMaskedBits || !row_live) ? 0.f : lo_f(e2);
       const float e1 = (a[k + 1] == kMaskedBits || !row_live) ? 0.f : hi_f(e2);
@@ -327,8 +295,8 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
   sum = lo_f(rs) + hi_f(rs);
 }
 
-template <int D, bool CAUSAL, bool F16, bool QK16, int NG, bool PV8>
-__global__ void __launch_bounds__(Roles<NG>::THREADS, 2 / NG)
+template <int D, bool CAUSAL, bool F16, bool QK16, bool PV8>
+__global__ void __launch_bounds__(THREADS, 2)
 k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
   using L = Smem<D, QK16, PV8>;
@@ -343,84 +311,22 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   // FP8 P~ (f4) is rounded relative to the reference max: rescale eagerly so
   // the reference is the true running max (R27), as the oracle's P~ = e^{S-m}
   constexpr float kRefThreshold = PV8 ? 0.0f : (F16 ? kRescaleThresholdF16 : kRescaleThreshold);
-  using R = Roles<NG>;
   constexpr int KST = L::KST, VST = L::VST;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem0 = reinterpret_cast<unsigned char*>(
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
+  // `warp` comes from a shuffle, so the compiler treats it (and every smem /
+  // barrier / TMEM address derived from it) as warp-uniform
   const int warp = __shfl_sync(0xffffffffu, warp_id(), 0), lane = lane_id();
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem0 + L::OFF_MISC);   // group 0's
-  // NG = 1: this CTA's work item comes from the LPT list of k_order (the
-  // items with the most kept blocks launch first); NG = 2 (experiment): two
-  // query tiles of head blockIdx.y
-  int bhq = static_cast<int>(blockIdx.y), i_item = 0;
-  if (NG == 1) {
-    const int item = __ldg(p.order + blockIdx.x);
-    bhq = item / p.T_m;
-    i_item = item - bhq * p.T_m;
-  }
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  // this CTA's work item from the launch order of k_order (the items with
+  // the most kept blocks launch first)
+  const int item = __ldg(p.order + blockIdx.x);
+  const int bhq = item / p.T_m, i = item - bhq * p.T_m;
   const int b = bhq / p.Hq, hq = bhq % p.Hq;
   const int bkv = b * p.Hkv + hq / p.group;
-  // query tile of group gg: u = blockIdx.x * NG + gg in launch order (causal:
-  // longest rows first); u >= T_m (odd T_m, last pair) is an empty group
-  auto tile_of = [&](int gg, int& i_out) -> int {
-    if (NG == 1) {
-      i_out = i_item;
-      return p.cnt[static_cast<int64_t>(bhq) * p.T_m + i_item];
-    }
-    const int u = static_cast<int>(blockIdx.x) * NG + gg;
-    if (u >= p.T_m) { i_out = p.T_m; return 0; }
-    i_out = CAUSAL ? (p.T_m - 1 - u) : u;
-    return p.cnt[static_cast<int64_t>(bhq) * p.T_m + i_out];
-  };
 
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int gg = 0; gg < NG; ++gg) {
-      uint64_t* bg = reinterpret_cast<uint64_t*>(smem0 + gg * L::GROUP + L::OFF_BAR);
-      mbar_init(bg, 1);                                                  // q_full
-      for (int s = 0; s < KST; ++s) { mbar_init(bg + 1 + s, 1); mbar_init(bg + 1 + KST + s, 1); }
-      for (int s = 0; s < VST; ++s) {
-        mbar_init(bg + 1 + 2 * KST + s, 1);
-        mbar_init(bg + 1 + 2 * KST + VST + s, 1);
-      }
-      uint64_t* sf = bg + 1 + 2 * KST + 2 * VST;
-      for (int s = 0; s < L::NSB; ++s) {
-        mbar_init(sf + s, 1);               // s_full
-        mbar_init(sf + L::NSB + s, NSOFT);  // p_full
-        mbar_init(sf + 2 * L::NSB + s, 1);  // o_tail
-      }
-    }
-    fence_mbar_init();
-  }
-  if constexpr (L::BIAS) {
-    // constant operands of the bias MMA (every element equal, so the core
-    // matrix layout of the descriptor is immaterial)
-    constexpr uint32_t kOnes = kBf16One | (static_cast<uint32_t>(kBf16One) << 16);
-    constexpr uint32_t kParts = kBf16MagicPart | (static_cast<uint32_t>(kBf16MagicPart) << 16);
-#pragma unroll
-    for (int gg = 0; gg < NG; ++gg) {
-      uint32_t* cw = reinterpret_cast<uint32_t*>(smem0 + gg * L::GROUP + L::OFF_CA);
-      for (int x = threadIdx.x; x < (L::CA_BYTES + L::CB_BYTES) / 4; x += blockDim.x)
-        cw[x] = x < L::CA_BYTES / 4 ? kOnes : kParts;
-    }
-    fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
-  }
-  if (warp == R::MMA0) tmem_alloc<256 * NG>(tmem_base_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_base_slot;
-
-  // group of this warp: softmax warps 4g..4g+3, producer LOAD0+g, MMA MMA0+g.
-  // `warp` comes from a shuffle, so the compiler treats it (and g, and every
-  // smem / barrier / TMEM address derived from it) as warp-uniform; one copy
-  // of the code serves both groups (two copies thrash the instruction cache).
-  const int g = (NG == 1) ? 0
-                          : (warp < R::SOFT ? (warp >> 2)
-                                            : (warp < R::MMA0 ? warp - R::LOAD0 : warp - R::MMA0));
-  unsigned char* smem = smem0 + g * L::GROUP;
   int8_t* sQ = reinterpret_cast<int8_t*>(smem + L::OFF_Q);
   int8_t* sK = reinterpret_cast<int8_t*>(smem + L::OFF_K);
   unsigned char* sV = smem + L::OFF_V;
@@ -435,17 +341,43 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   uint64_t* p_full = s_full + NSB;           // [NSB]
   uint64_t* o_tail = p_full + NSB;           // [NSB], each completes once
   uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC) + 1;       // [NSB][4]
-  int i = 0, i_other = 0;
-  const int n_tiles = tile_of(g, i);
-  const int n_other = (NG == 2) ? tile_of(g ^ 1, i_other) : 0;
-  const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + min(i, p.T_m - 1);
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KST; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+    for (int s = 0; s < VST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
+    for (int s = 0; s < NSB; ++s) {
+      mbar_init(s_full + s, 1);
+      mbar_init(p_full + s, NSOFT);
+      mbar_init(o_tail + s, 1);
+    }
+    fence_mbar_init();
+  }
+  if constexpr (L::BIAS) {
+    // constant operands of the bias MMA (every element equal, so the core
+    // matrix layout of the descriptor is immaterial)
+    constexpr uint32_t kOnes = kBf16One | (static_cast<uint32_t>(kBf16One) << 16);
+    constexpr uint32_t kParts = kBf16MagicPart | (static_cast<uint32_t>(kBf16MagicPart) << 16);
+    uint32_t* cw = reinterpret_cast<uint32_t*>(smem + L::OFF_CA);
+    for (int x = threadIdx.x; x < (L::CA_BYTES + L::CB_BYTES) / 4; x += blockDim.x)
+      cw[x] = x < L::CA_BYTES / 4 ? kOnes : kParts;
+    fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
+  }
+  if (warp == WARP_MMA) tmem_alloc<256>(tmem_base_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + i;
+  const int n_tiles = p.cnt[row_id];
   const int32_t* lut_row = p.lut + row_id * p.T_n;
-  const uint32_t tS0 = tmem_base + g * 256, tO = tS0 + NSB * BK;
+  const uint32_t tS0 = tmem_base, tO = tS0 + NSB * BK;
   // P~V(u) of the last NSB tiles, u >= n - NSB, completes o_tail[u - max(0,
   // n - NSB)] -- a barrier used once, so its parity-0 wait is unambiguous
   auto wait_tail = [&](int u) { mbar_wait(o_tail + (u - max(0, n_tiles - NSB)), 0); };
 
-  if (warp >= R::LOAD0 && warp < R::MMA0) {
+  if (warp == WARP_LOAD) {
     // ============================ TMA producer ============================
     if (lane == 0 && n_tiles > 0) {
       tma_prefetch_desc(&tmQ);
@@ -464,14 +396,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         if (t + 1 < n_tiles) j_next = __ldg(lut_row + t + 1);
         const int ks = t % KST;
         mbar_wait(k_empty + ks, ((t / KST) & 1) ^ 1);
-#ifdef SPARGE_ABL_NOLOAD   // timing ablation only (wrong results): loads for the first ring pass only
-        if (t >= 4) {
-          mbar_arrive(k_full + ks);
-          mbar_wait(v_empty + t % VST, ((t / VST) & 1) ^ 1);
-          mbar_arrive(v_full + t % VST);
-          continue;
-        }
-#endif
         mbar_arrive_expect_tx(k_full + ks, L::K_BYTES);
         if (QK16) {
 #pragma unroll
@@ -486,7 +410,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
       }
     }
-  } else if (warp >= R::MMA0) {
+  } else if (warp == WARP_MMA) {
     // ============================ MMA issuer ==============================
     if (lane == 0 && n_tiles > 0) {
       constexpr uint32_t IDESC_QK =
@@ -519,9 +443,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
-#ifdef SPARGE_ABL_NOPV   // timing ablation only (wrong results): one P~V MMA instead of four
-              if (kk == 0)
-#endif
               mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
           }
           ++issued;
@@ -600,16 +521,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       cj = __ldg(lut_row + lane);
       cc_ = dq_scale * __ldg(dk_row + cj);
     }
-    // Pair mode (NG = 2): the exp phases of the two warps that share an SMSP
-    // (warp quad of group 0 and of group 1) alternate strictly -- a bar.sync
-    // / bar.arrive hand-off on barriers 1+quad+4g -- so one warp's MUFU burst
-    // overlaps the other's per-tile bookkeeping instead of contending for the
-    // same MUFU.  Both run max(n_0, n_1) hand-off rounds (a finished group
-    // keeps passing the token), group 1 starts by handing the token to group 0.
-    const uint32_t my_bar = 1 + quad + 4 * g, other_bar = 1 + quad + 4 * (g ^ 1);
-    constexpr bool PP = NG == 2 && kPingPong;
-    const int n_iter = PP ? max(n_tiles, n_other) : n_tiles;
-    if (PP && g == 1 && n_iter > 0) named_bar_arrive(other_bar, 64);
 #ifdef SPARGE_PHASE_TIMING
     long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
     long long ph_last = clock64();
@@ -638,16 +549,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 
         PT_MARK(0);
         mbar_wait(s_full + sb, (t / NSB) & 1);
-#ifdef SPARGE_ABL_NOSOFT   // timing ablation only (wrong results): MMA/sync pipeline floor
-        tc_fence_after();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(pv_flag + sb * 4 + quad)), "r"(1u) : "memory");
-          mbar_arrive(p_full + sb);
-        }
-        continue;
-#endif
         PT_MARK(1);
         tc_fence_after();
         tmem_ld32(tS, reinterpret_cast<uint32_t*>(a));
@@ -691,12 +592,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             for (int k = 16; k < BK; k += 16)
 #pragma unroll
               for (int u = 0; u < 8; ++u) m8[u] = max(m8[u], max(a[k + u], a[k + 8 + u]));
-#ifdef SPARGE_ABL_NOMAX   // timing ablation only (wrong results): no max tree
-            const int mx = max(a[0], a[63]);
-#else
             const int mx = max(max(max(m8[0], m8[1]), max(m8[2], m8[3])),
                                max(max(m8[4], m8[5]), max(m8[6], m8[7])));
-#endif
             // S = acc * dq * dk / sqrt(d) in log2 units; exact int -> fp32
             // through the magic constant (I2F runs on the slow XU pipe)
             row_has = mx != kMaskedBits;
@@ -707,26 +604,14 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         // factor, so O = acc * s_c / l needs no extra scale)
         constexpr float kPvShift = PV8 ? 7.0f : 0.0f;
         float m_loc, rsum = 0.f;
-        bool row_has, have_exps = false;
-        if (kSpec && !need_mask) {
-          // Speculative P~ with the current reference max: with the lazy
-          // reference (R22) it stays put on almost every tile, so the exps
-          // need not wait for the row max -- the max tree and the exps form
-          // one basic block and interleave.  A fresh row (reference -inf)
-          // yields inf here and is recomputed below.
-          exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
-          row_max(m_loc, row_has);
-          have_exps = true;
-        } else {
-          row_max(m_loc, row_has);
-        }
+        bool row_has;
+        row_max(m_loc, row_has);
         const float m_new = fmaxf(m_true, m_loc);
         // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
         compute = __any_sync(0xffffffffu, row_has && (m_loc - m_new > p.lam2));
         // lazy rescale (R22): move the reference max only when it lags the
         // true max by more than the threshold (always when it is -inf)
         need = compute && (m_new > m_ref + kRefThreshold);
-        const bool redo = __any_sync(0xffffffffu, need) || !have_exps;
         rescale_o = __any_sync(0xffffffffu, need && (m_ref > -INFINITY));
         if (need) {
           alpha = ex2_approx(m_ref - m_new);   // 0 when m_ref = -inf (l, O are 0 then)
@@ -736,15 +621,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         m_true = m_new;
         PT_MARK(2);
 
-        if (PP) named_bar_sync(my_bar, 64);
         // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ (l.13) ----
-        if (redo) {
-          if (need_mask || kSpec) exps64<true, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
-          else exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
-        }
+        if (need_mask) exps64<true, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
+        else exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
         l += rsum;           // R9: skipped groups still add their mass to l
       }
-      if (PP && !(g == 1 && t == n_iter - 1)) named_bar_arrive(other_bar, 64);
 
       {
         if (!compute) {
@@ -790,11 +671,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         if (compute) ++slices;
         PT_MARK(5);
       }
-    }
-    // this group is done: keep passing the token while the other one works
-    for (int t = n_tiles; PP && t < n_iter; ++t) {
-      named_bar_sync(my_bar, 64);
-      if (!(g == 1 && t == n_iter - 1)) named_bar_arrive(other_bar, 64);
     }
 #ifdef SPARGE_PHASE_TIMING
     if (lane == 0 && p.phase_clk)
@@ -845,10 +721,10 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == R::MMA0) {
+  if (warp == WARP_MMA) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc<256 * NG>(tmem_base);
+    tmem_dealloc<256>(tmem_base);
   }
 #ifdef SPARGE_CTA_TIMING
   if (threadIdx.x == 0) CTA_REC(3, gtimer());
@@ -858,13 +734,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 template <int D, bool CAUSAL, bool F16, bool QK16, bool PV8 = false>
 cudaError_t launch_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                      const AttnParams& p, int B, cudaStream_t stream) {
-  constexpr int NG = kPairs ? 2 : 1;
-  auto kern = k_sparse_attn<D, CAUSAL, F16, QK16, NG, PV8>;
-  const int smem = NG * Smem<D, QK16, PV8>::GROUP + 1024;   // + slack for 1024-B alignment
+  auto kern = k_sparse_attn<D, CAUSAL, F16, QK16, PV8>;
+  const int smem = Smem<D, QK16, PV8>::BYTES + 1024;   // + slack for 1024-B alignment
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(NG == 1 ? p.T_m * B * p.Hq : (p.T_m + NG - 1) / NG, NG == 1 ? 1 : B * p.Hq);
-  kern<<<grid, Roles<NG>::THREADS, smem, stream>>>(mq, mk, mv, p);
+  kern<<<dim3(p.T_m * B * p.Hq), THREADS, smem, stream>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
 
@@ -918,9 +792,8 @@ namespace sparge {
 #endif
 
 int attn_smem_bytes(int d, int qk16) {
-  const int ng = kPairs ? 2 : 1;
-  if (qk16) return ng * (d == 128 ? Smem<128, true>::GROUP : Smem<64, true>::GROUP) + 1024;
-  return ng * (d == 128 ? Smem<128, false>::GROUP : Smem<64, false>::GROUP) + 1024;
+  if (qk16) return (d == 128 ? Smem<128, true>::BYTES : Smem<64, true>::BYTES) + 1024;
+  return (d == 128 ? Smem<128, false>::BYTES : Smem<64, false>::BYTES) + 1024;
 }
 
 }  // namespace sparge
