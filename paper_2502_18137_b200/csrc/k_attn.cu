@@ -93,7 +93,15 @@ constexpr float kMagicF = 12582912.0f;
 #ifndef SPARGE_POLY_EVERY
 #define SPARGE_POLY_EVERY 0
 #endif
-constexpr int kPolyEvery = SPARGE_POLY_EVERY;   // one pair in kPolyEvery uses exp2_poly2 (0: none)
+// one pair in kPolyEvery uses exp2_poly2 (0: none).  d = 128 is chain-bound
+// (the MUFU is not the limit: 0); the d = 64 kernel has half the tensor work
+// per tile and is softmax-bound, where offloading 1 pair in 8 measured ~1 %
+// faster (CogVideoX) and 1 in 4 slower
+#ifndef SPARGE_POLY_EVERY64
+#define SPARGE_POLY_EVERY64 8
+#endif
+constexpr int kPolyEvery = SPARGE_POLY_EVERY;
+constexpr int kPolyEvery64 = SPARGE_POLY_EVERY64;
 
 // CTA roles: softmax warps 0-3 (one per TMEM lane quadrant), TMA producer
 // warp 4, MMA issuer warp 5.  (Experiments with two query tiles per CTA, a
@@ -258,7 +266,8 @@ struct SBits {
   static constexpr int kMasked = QK16 ? static_cast<int>(0xFF800000u) : (BIAS ? 0 : INT_MIN);
 };
 
-template <bool MASKED, bool F16, bool QK16 = false, bool PV8 = false, bool BIAS = false>
+template <bool MASKED, bool F16, bool QK16 = false, bool PV8 = false, bool BIAS = false,
+          int POLY = 0>
 __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, uint32_t* pw,
                                        float& sum) {
   constexpr int kAdd = SBits<QK16, BIAS>::kAdd;
@@ -273,7 +282,7 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
     const uint64_t x2 = fma2(pk(__int_as_float(a[k] + kAdd), __int_as_float(a[k + 1] + kAdd)),
                              c2, nb2);
     uint64_t e2;
-    if (!MASKED && kPolyEvery > 0 && ((k >> 1) % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
+    if (!MASKED && POLY > 0 && ((k >> 1) % (POLY > 0 ? POLY : 1)) == POLY - 1)
       e2 = exp2_poly2(x2);
     else
       e2 = pk(ex2_approx(lo_f(x2)), ex2_approx(hi_f(x2)));
@@ -622,8 +631,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         PT_MARK(2);
 
         // ---- P~ = exp2(S*log2e - m_ref), row sum, 16-bit P~ (l.13) ----
-        if (need_mask) exps64<true, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
-        else exps64<false, F16, QK16, PV8, L::BIAS>(a, c, m_ref - kPvShift, pw, rsum);
+        constexpr int kPoly = D == 64 ? kPolyEvery64 : kPolyEvery;
+        if (need_mask) exps64<true, F16, QK16, PV8, L::BIAS, kPoly>(a, c, m_ref - kPvShift, pw, rsum);
+        else exps64<false, F16, QK16, PV8, L::BIAS, kPoly>(a, c, m_ref - kPvShift, pw, rsum);
         l += rsum;           // R9: skipped groups still add their mass to l
       }
 
