@@ -152,7 +152,7 @@ struct Smem {
   // third buffer measured no faster on CogVideoX (1.067 vs 1.058 ms: the
   // d = 64 kernel is softmax-bound), so SPARGE_NSB64 = 3 is an option only
   static constexpr int NSB = SPARGE_NSB64 > 0 && D == 64 ? SPARGE_NSB64 : 2;
-  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 3 * 3;
+  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 3;
   static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;    // [0] TMEM base, [1..8] pv flags
   static constexpr int TOTAL = OFF_MISC + 64;
   static constexpr int BYTES = (TOTAL + 1023) / 1024 * 1024;
@@ -342,21 +342,21 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = k_full + KST;
-  uint64_t* v_full = k_empty + KST;
+  // s_full[ks]: QK of the tile in K slot ks is done -- S is ready for the
+  // softmax AND the K slot is free for the producer (one commit, not two)
+  uint64_t* s_full = k_full + KST;           // [KST]
+  uint64_t* v_full = s_full + KST;
   uint64_t* v_empty = v_full + VST;
   constexpr int NSB = L::NSB;
-  uint64_t* s_full = v_empty + VST;          // [NSB]
-  uint64_t* p_full = s_full + NSB;           // [NSB]
+  uint64_t* p_full = v_empty + VST;          // [NSB]
   uint64_t* o_tail = p_full + NSB;           // [NSB], each completes once
   uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC) + 1;       // [NSB][4]
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < KST; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+    for (int s = 0; s < KST; ++s) { mbar_init(k_full + s, 1); mbar_init(s_full + s, 1); }
     for (int s = 0; s < VST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
     for (int s = 0; s < NSB; ++s) {
-      mbar_init(s_full + s, 1);
       mbar_init(p_full + s, NSOFT);
       mbar_init(o_tail + s, 1);
     }
@@ -404,7 +404,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         const int j = j_next;
         if (t + 1 < n_tiles) j_next = __ldg(lut_row + t + 1);
         const int ks = t % KST;
-        mbar_wait(k_empty + ks, ((t / KST) & 1) ^ 1);
+        mbar_wait(s_full + ks, ((t / KST) & 1) ^ 1);     // QK(t - KST) done: slot free
         mbar_arrive_expect_tx(k_full + ks, L::K_BYTES);
         if (QK16) {
 #pragma unroll
@@ -488,8 +488,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           for (int kk = 0; kk < D / 32; ++kk)       // K = 32 per kind::i8 MMA (32 B)
             mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, (L::BIAS || kk > 0) ? 1u : 0u);
         }
-        tc_commit(s_full + sb);
-        tc_commit(k_empty + ks);
+        tc_commit(s_full + ks);
       };
       for (int t = 0; t < NSB - 1 && t < n_tiles; ++t) issue_qk(t);
       for (int t = 0; t < n_tiles; ++t) {
@@ -557,7 +556,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         c = __shfl_sync(0xffffffffu, cc_, tl);
 
         PT_MARK(0);
-        mbar_wait(s_full + sb, (t / NSB) & 1);
+        mbar_wait(s_full + t % KST, (t / KST) & 1);
         PT_MARK(1);
         tc_fence_after();
         tmem_ld32(tS, reinterpret_cast<uint32_t*>(a));
@@ -649,7 +648,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           // issued P~V, then rescale in TMEM (before p_full(t) releases P~V(t)).
           if (t >= 1) {
             const int tq = t + NSB - 1;
-            if (tq < n_tiles) mbar_wait(s_full + tq % NSB, (tq / NSB) & 1);
+            if (tq < n_tiles) mbar_wait(s_full + tq % KST, (tq / KST) & 1);
             else wait_tail(t - 1);   // P~V(t-1)
           }
           tc_fence_after();

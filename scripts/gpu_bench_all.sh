@@ -5,7 +5,7 @@ set -u
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?; tail -1 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --steps 30 --warmup 5 --out gpurun_out/bench.json > gpurun_out/bench.log 2>&1; echo bench_rc=$?
-for w in cogvideox_2b mochi sweep_8k sweep_32k sweep_128k; do
+for w in cogvideox_2b mochi mochi_22k sweep_8k sweep_16k sweep_32k sweep_64k sweep_128k; do
   timeout 900 python bench.py --workload $w --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --out gpurun_out/bench_$w.json > gpurun_out/bench_$w.log 2>&1; echo ${w}_rc=$?
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo ref_rc=$?
