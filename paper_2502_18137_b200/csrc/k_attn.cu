@@ -152,7 +152,7 @@ struct Smem {
   // third buffer measured no faster on CogVideoX (1.067 vs 1.058 ms: the
   // d = 64 kernel is softmax-bound), so SPARGE_NSB64 = 3 is an option only
   static constexpr int NSB = SPARGE_NSB64 > 0 && D == 64 ? SPARGE_NSB64 : 2;
-  static constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 * 3;
+  static constexpr int N_BARS = 1 + 2 * KST + VST + 2 * 3;
   static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;    // [0] TMEM base, [1..8] pv flags
   static constexpr int TOTAL = OFF_MISC + 64;
   static constexpr int BYTES = (TOTAL + 1023) / 1024 * 1024;
@@ -346,16 +346,15 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   // softmax AND the K slot is free for the producer (one commit, not two)
   uint64_t* s_full = k_full + KST;           // [KST]
   uint64_t* v_full = s_full + KST;
-  uint64_t* v_empty = v_full + VST;
   constexpr int NSB = L::NSB;
-  uint64_t* p_full = v_empty + VST;          // [NSB]
+  uint64_t* p_full = v_full + VST;           // [NSB]
   uint64_t* o_tail = p_full + NSB;           // [NSB], each completes once
   uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC) + 1;       // [NSB][4]
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < KST; ++s) { mbar_init(k_full + s, 1); mbar_init(s_full + s, 1); }
-    for (int s = 0; s < VST; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
+    for (int s = 0; s < VST; ++s) mbar_init(v_full + s, 1);
     for (int s = 0; s < NSB; ++s) {
       mbar_init(p_full + s, NSOFT);
       mbar_init(o_tail + s, 1);
@@ -414,7 +413,13 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           tma_load_3d(sK + ks * L::K_BYTES, &tmK, k_full + ks, 0, j * BK, bkv);
         }
         const int vs = t % VST;
-        mbar_wait(v_empty + vs, ((t / VST) & 1) ^ 1);
+        // V slot of tile t - VST is free once P~V(t - VST) is done, i.e. once
+        // QK(t - VST + 2) -- issued after it -- is (its s_full commit covers
+        // every earlier MMA; a skipped P~V needs nothing)
+        if (t >= VST) {
+          const int u = t - VST + 2;
+          mbar_wait(s_full + u % KST, (u / KST) & 1);
+        }
         mbar_arrive_expect_tx(v_full + vs, L::V_BYTES);
         tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
       }
@@ -456,7 +461,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           }
           ++issued;
         }
-        tc_commit(v_empty + vs);
         // only the last NSB P~V signal completion (o_tail): the softmax's
         // rare O rescale at tile t waits on s_full(t+NSB-1) instead (QK(t+NSB-1)
         // is issued after P~V(t-1)) while that tile exists, else on o_tail, as
