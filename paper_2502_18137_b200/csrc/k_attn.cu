@@ -153,8 +153,9 @@ struct Smem {
   // d = 64 kernel is softmax-bound), so SPARGE_NSB64 = 3 is an option only
   static constexpr int NSB = SPARGE_NSB64 > 0 && D == 64 ? SPARGE_NSB64 : 2;
   static constexpr int N_BARS = 1 + 2 * KST + VST + 2 * 3;
-  static constexpr int OFF_MISC = OFF_BAR + N_BARS * 8;    // [0] TMEM base, [1..8] pv flags
-  static constexpr int TOTAL = OFF_MISC + 64;
+  // [0] TMEM base, [16..] P~V flags [NSB][4]
+  static constexpr int OFF_MISC = (OFF_BAR + N_BARS * 8 + 15) / 16 * 16;
+  static constexpr int TOTAL = OFF_MISC + 16 + 16 * NSB;
   static constexpr int BYTES = (TOTAL + 1023) / 1024 * 1024;
   // INT8: one K-atom of D bytes per row (128 -> SW128, 64 -> SW64); 16-bit:
   // 128-B atoms, the second (d = 128) BQ*128 / BK*128 bytes after the first
@@ -349,7 +350,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   constexpr int NSB = L::NSB;
   uint64_t* p_full = v_full + VST;           // [NSB]
   uint64_t* o_tail = p_full + NSB;           // [NSB], each completes once
-  uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC) + 1;       // [NSB][4]
+  // P~V flags [NSB][4] (16-B aligned rows: one ld.shared.v4 per tile)
+  uint32_t* pv_flag = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC + 16);
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -443,8 +445,11 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         mbar_wait(p_full + pb, (u / NSB) & 1);
         mbar_wait(v_full + vs, (u / VST) & 1);
         tc_fence_after();
-        const bool any = (pv_flag[pb * 4 + 0] | pv_flag[pb * 4 + 1] |
-                          pv_flag[pb * 4 + 2] | pv_flag[pb * 4 + 3]) != 0;
+        uint32_t f0, f1, f2, f3;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(f0), "=r"(f1), "=r"(f2), "=r"(f3) : "r"(smem_u32(pv_flag + pb * 4))
+                     : "memory");
+        const bool any = (f0 | f1 | f2 | f3) != 0;
         if (any) {
           const uint32_t tP = tS0 + pb * BK;     // P~ 16-bit (32 cols) or e4m3 (16 cols)
           if (PV8) {
