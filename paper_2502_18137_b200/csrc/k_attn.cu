@@ -434,6 +434,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       // (kind::f8f6f4 with E4M3 A/B and fp32 D has the f16 field values)
       constexpr uint32_t IDESC_PV = (F16 || PV8) ? idesc_f16(BQ, D) : idesc_bf16(BQ, D);
       const uint64_t dQ = umma_desc_kmajor(smem_u32(sQ), L::ROW_BYTES_QK);
+      const uint64_t dK0 = umma_desc_kmajor(smem_u32(sK), L::ROW_BYTES_QK);
+      const uint64_t dV0 = umma_desc_kmajor(smem_u32(sV), PV8 ? 64 : 128);
       constexpr uint32_t IDESC_BIAS = idesc_bf16(BQ, BK);
       const uint64_t dCA = umma_desc_noswz(smem_u32(smem + L::OFF_CA), 128, 256);
       const uint64_t dCB = umma_desc_noswz(smem_u32(smem + L::OFF_CB), 128, 256);
@@ -454,12 +456,12 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           const uint32_t tP = tS0 + pb * BK;     // P~ 16-bit (32 cols) or e4m3 (16 cols)
           if (PV8) {
             // K = 32 e4m3 per kind::f8f6f4 MMA: 8 TMEM cols of P~, 32 B of V^T rows
-            const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 64);
+            const uint64_t dV = dV0 + static_cast<uint64_t>((vs * L::V_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < BK / 32; ++kk)
               mma_f8_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
           } else {
-            const uint64_t dV = umma_desc_kmajor(smem_u32(sV + vs * L::V_BYTES), 128);
+            const uint64_t dV = dV0 + static_cast<uint64_t>((vs * L::V_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)   // K = 16 per kind::f16 MMA: 8 TMEM cols
               mma_f16_ts(tO, tP + 8 * kk, dV + 2 * kk, IDESC_PV, 1u);
@@ -482,7 +484,9 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         const int ks = t % KST, sb = t % NSB;
         mbar_wait(k_full + ks, (t / KST) & 1);
         tc_fence_after();
-        const uint64_t dK = umma_desc_kmajor(smem_u32(sK + ks * L::K_BYTES), L::ROW_BYTES_QK);
+        // slot descriptors = the slot-0 descriptor + the slot offset in the
+        // 14-bit start-address field (smem < 256 KB: no carry out of it)
+        const uint64_t dK = dK0 + static_cast<uint64_t>((ks * L::K_BYTES) >> 4);
         if (QK16) {
           // K = 16 per kind::f16 MMA (32 B): 4 steps per 128-B atom, then
           // the next atom (fp32 S accumulators)
