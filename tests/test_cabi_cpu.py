@@ -42,6 +42,11 @@ def test_strerror_and_validation_without_gpu(sp):
     assert sp._lib.sparge_attn_workspace(ctypes.byref(bad)) == 0
     bad = sp.make_shape(1, 1, 1, 128, 96)           # d not in {64,128}
     assert sp._lib.sparge_attn_workspace(ctypes.byref(bad)) == 0
+    for degenerate in (sp.make_shape(1, 1, 1, 0, 128), sp.make_shape(0, 1, 1, 64, 128),
+                       sp.make_shape(1, 0, 1, 64, 64)):   # empty inputs are rejected (N >= 1, B, H >= 1)
+        assert sp._lib.sparge_attn_workspace(ctypes.byref(degenerate)) == 0
+        assert sp._lib.sparge_predict_mask(ctypes.byref(degenerate), None, None, None, None, 0.9, 0.5,
+                                           None, None, None, None, 0, None) == sp.SPARGE_EINVAL
     good = sp.make_shape(2, 4, 2, 1000, 128)
     # status + V^T [B, Hkv, d, N_pad] bf16 + launch order of B*Hq*T_m int32 items + its scratch (256-B rounded)
     assert sp._lib.sparge_attn_workspace(ctypes.byref(good)) == 256 + 2 * 2 * 128 * 1024 * 2 + 256 + 512
