@@ -32,7 +32,12 @@ namespace {
 
 // ---------------------------------------------------------------- S^ GEMM
 constexpr int kTile = 64;          // query blocks x key blocks per CTA
-constexpr int kGemmThreads = 256;  // 8 warps, one 8-row strip each
+#ifdef SPARGE_SHAT_8WARPS
+constexpr int kColSplit = 1;       // 8 warps, one 8-row strip x 64 keys each
+#else
+constexpr int kColSplit = 2;       // 16 warps, one 8-row strip x 32 keys each
+#endif
+constexpr int kGemmThreads = 256 * kColSplit;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
@@ -78,28 +83,30 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 
-  // warp wid: rows 8*wid..8*wid+7 against all 64 keys (8 DMMA tiles)
-  // fragments (m8n8k4, f64): A row = lane/4, k = lane%4; B k = lane%4,
-  // n = lane/4; C row = lane/4, cols 2*(lane%4) + {0,1}
+  // warp wid: rows 8*(wid%8)..+7 against keys [cq*NKT*8, (cq+1)*NKT*8),
+  // cq = wid/8 (NKT DMMA tiles); fragments (m8n8k4, f64): A row = lane/4,
+  // k = lane%4; B k = lane%4, n = lane/4; C row = lane/4, cols 2*(lane%4) + {0,1}
+  constexpr int NKT = 8 / kColSplit;
+  const int strip = wid & 7, cq = wid >> 3;
   const int g = lane >> 2, t4 = lane & 3;
-  double acc[8][2];
+  double acc[NKT][2];
 #pragma unroll
-  for (int kt = 0; kt < 8; ++kt) acc[kt][0] = acc[kt][1] = 0.0;
-  const double* arow = sq + (8 * wid + g) * KR + t4;
-  const double* brow = sk + g * KR + t4;
+  for (int kt = 0; kt < NKT; ++kt) acc[kt][0] = acc[kt][1] = 0.0;
+  const double* arow = sq + (8 * strip + g) * KR + t4;
+  const double* brow = sk + (cq * NKT * 8 + g) * KR + t4;
 #pragma unroll 4
   for (int ks = 0; ks < D / 4; ++ks) {
     const double a = arow[4 * ks];
 #pragma unroll
-    for (int kt = 0; kt < 8; ++kt) dmma_884(acc[kt][0], acc[kt][1], a, brow[8 * kt * KR + 4 * ks]);
+    for (int kt = 0; kt < NKT; ++kt) dmma_884(acc[kt][0], acc[kt][1], a, brow[8 * kt * KR + 4 * ks]);
   }
   const double inv_sqrt_d = 1.0 / sqrt(static_cast<double>(D));
-  const int row = i0 + 8 * wid + g;
+  const int row = i0 + 8 * strip + g;
   if (row < T_m) {
     double* out = shat + (qbase + row) * T_n;
 #pragma unroll
-    for (int kt = 0; kt < 8; ++kt) {
-      const int key = j0 + 8 * kt + 2 * t4;
+    for (int kt = 0; kt < NKT; ++kt) {
+      const int key = j0 + cq * NKT * 8 + 8 * kt + 2 * t4;
       if (key < T_n) out[key] = acc[kt][0] * inv_sqrt_d;
       if (key + 1 < T_n) out[key + 1] = acc[kt][1] * inv_sqrt_d;
     }
@@ -431,12 +438,37 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   constexpr bool padded = RS > 0;
   auto kix = [&](int j) { return padded ? pidx(j) : j; };
   double mx = -INFINITY;
+#ifdef SPARGE_TOPCDF_SERIAL_LOADS
   for (int j = lane; j < T_n; j += 32) {
     const bool dead = causal && (j * bk > last_q);
     const double s = (dead || k_sim[kbase + j] < theta) ? -INFINITY : srow[j];
     key[kix(j)] = s;
     mx = fmax(mx, s);
   }
+#else
+  // the row's global loads batched kLoadBatch deep (the smem stores between
+  // them would otherwise serialise one load latency per 32 entries)
+  constexpr int kLoadBatch = 8;
+  for (int j0 = lane; j0 < T_n; j0 += 32 * kLoadBatch) {
+    double sv[kLoadBatch], kv[kLoadBatch];
+#pragma unroll
+    for (int u = 0; u < kLoadBatch; ++u) {
+      const int j = j0 + 32 * u;
+      sv[u] = (j < T_n) ? __ldg(srow + j) : 0.0;
+      kv[u] = (j < T_n) ? __ldg(k_sim + kbase + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kLoadBatch; ++u) {
+      const int j = j0 + 32 * u;
+      if (j < T_n) {
+        const bool dead = causal && (j * bk > last_q);
+        const double s = (dead || kv[u] < theta) ? -INFINITY : sv[u];
+        key[kix(j)] = s;
+        mx = fmax(mx, s);
+      }
+    }
+  }
+#endif
   mx = warp_max(mx);
   const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
 
