@@ -189,8 +189,9 @@ int sparge_predict_mask(const sparge_shape* shape,
 size_t sparge_predict_workspace(const sparge_shape* shape);
 
 /* Bytes of device workspace sparge_attn_fwd needs for `shape`: the status
- * word (256 B), the V^T staging (16-bit, or E4M3 for pv_dtype FP8, rounded
- * to 256 B), for FP8 the per-channel amax and dequant scales, and the launch
+ * word (256 B), the V^T staging (16-bit tile-major [B, Hkv, N_pad/64, d, 64],
+ * or E4M3 row-major [B, Hkv, d, N_pad] for pv_dtype FP8; N_pad = N rounded
+ * up to 64; rounded to 256 B), for FP8 the per-channel amax and dequant scales, and the launch
  * order of the B*Hq*T_m attention work items (int32, longest first; rounded
  * to 256 B).  0 on invalid shape. */
 size_t sparge_attn_workspace(const sparge_shape* shape);

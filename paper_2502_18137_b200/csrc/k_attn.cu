@@ -423,7 +423,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           mbar_wait(s_full + u % KST, (u / KST) & 1);
         }
         mbar_arrive_expect_tx(v_full + vs, L::V_BYTES);
-        tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
+        if (kVtTiled && !PV8) tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, 0, j * D, bkv);
+        else tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
       }
     }
   } else if (warp == WARP_MMA) {

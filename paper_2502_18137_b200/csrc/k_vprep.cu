@@ -1,8 +1,9 @@
 // k_vprep -- V staging for the P~V product of step a3.
 //
-// Writes V^T[b, hkv, c, r] = V[b, hkv, perm[r], c] (zero for r >= N) so that
-// every 64-key tile of V is a K-major UMMA B operand (64 keys = 128 bytes per
-// row, SWIZZLE_128B), loaded by one TMA box per kept tile.  The Hilbert
+// Writes V^T[b, hkv, r / 64, c, r % 64] = V[b, hkv, perm[r], c] (zero for
+// r >= N; tile-major, kVtTiled) so that every 64-key tile of V is a K-major
+// UMMA B operand (64 keys = 128 bytes per row, SWIZZLE_128B) stored as one
+// contiguous block and loaded by one TMA box per kept tile.  The Hilbert
 // gather of §3.7 is fused here.  Bound: HBM (2 B read + 2 B write
 // per element).
 #include <cuda_fp16.h>
@@ -51,7 +52,10 @@ k_vprep(const uint16_t* __restrict__ v, int64_t sb, int64_t sh, int64_t sn,
   __syncthreads();
   // write D rows x 64 keys: thread (c, k16) packs 16 keys (32 B); lanes run
   // over consecutive c, so the column reads of the tile are conflict-free
-  uint16_t* out = vt + ((static_cast<int64_t>(b) * Hkv + h) * D) * n_pad + jb * BK;
+  // tile-major: this CTA's 64-key tile is one contiguous [D][64] block
+  uint16_t* out = kVtTiled ? vt + ((static_cast<int64_t>(b) * Hkv + h) * (n_pad / BK) + jb) * D * BK
+                           : vt + ((static_cast<int64_t>(b) * Hkv + h) * D) * n_pad + jb * BK;
+  const int64_t row_stride = kVtTiled ? BK : n_pad;
 #pragma unroll
   for (int e = tid; e < D * (BK / 16); e += 256) {
     const int c = e % D, k16 = e / D;
@@ -60,7 +64,7 @@ k_vprep(const uint16_t* __restrict__ v, int64_t sb, int64_t sh, int64_t sn,
     for (int q = 0; q < 8; ++q)
       w[q] = static_cast<uint32_t>(tile[k16 * 16 + 2 * q][c]) |
              (static_cast<uint32_t>(tile[k16 * 16 + 2 * q + 1][c]) << 16);
-    uint4* o4 = reinterpret_cast<uint4*>(out + static_cast<int64_t>(c) * n_pad + k16 * 16);
+    uint4* o4 = reinterpret_cast<uint4*>(out + static_cast<int64_t>(c) * row_stride + k16 * 16);
     o4[0] = make_uint4(w[0], w[1], w[2], w[3]);
     o4[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }

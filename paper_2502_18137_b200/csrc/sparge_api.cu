@@ -264,9 +264,12 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
       !(pv8 ? encode3d(&mv, CU_TENSOR_MAP_DATA_TYPE_UINT8, vt, static_cast<uint64_t>(n_pad), d,
                        static_cast<uint64_t>(s.B) * s.Hkv, static_cast<uint64_t>(n_pad), d * n_pad,
                        64, s.d, CU_TENSOR_MAP_SWIZZLE_64B)
-            : encode3d(&mv, dt16, vt, static_cast<uint64_t>(n_pad), d,
-                       static_cast<uint64_t>(s.B) * s.Hkv, static_cast<uint64_t>(n_pad) * 2,
-                       d * n_pad * 2, 64, s.d, CU_TENSOR_MAP_SWIZZLE_128B)))
+            : (kVtTiled ? encode3d(&mv, dt16, vt, 64, d * static_cast<uint64_t>(n_pad / 64),
+                                   static_cast<uint64_t>(s.B) * s.Hkv, 128, d * n_pad * 2, 64, s.d,
+                                   CU_TENSOR_MAP_SWIZZLE_128B)
+                        : encode3d(&mv, dt16, vt, static_cast<uint64_t>(n_pad), d,
+                                   static_cast<uint64_t>(s.B) * s.Hkv, static_cast<uint64_t>(n_pad) * 2,
+                                   d * n_pad * 2, 64, s.d, CU_TENSOR_MAP_SWIZZLE_128B))))
     return SPARGE_ECUDA;
 
   // launch order: the longest items first, then groups of kv-heads whose

@@ -9,6 +9,16 @@
 
 namespace sparge {
 
+// 16-bit V^T staging layout: tile-major [B, Hkv, N_pad/64, d, 64] (each
+// 64-key tile one contiguous 16 KB (d=128) block: contiguous writes in
+// k_vprep, one TMA box per tile), or with -DSPARGE_VT_ROWMAJOR the
+// row-major [B, Hkv, d, N_pad] of v5.  The FP8 staging stays row-major.
+#ifdef SPARGE_VT_ROWMAJOR
+constexpr bool kVtTiled = false;
+#else
+constexpr bool kVtTiled = true;
+#endif
+
 // mu: nullptr, or (K only) the smoothing mean [B, Hkv, d] of k_smooth.cu:
 // the INT8 path quantises fl32(x - mu), the statistics use the raw x (R28, R14)
 cudaError_t launch_quant(const sparge_shape& s, const void* x, sparge_strides st, int is_key,

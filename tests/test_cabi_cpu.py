@@ -48,7 +48,7 @@ def test_strerror_and_validation_without_gpu(sp):
         assert sp._lib.sparge_predict_mask(ctypes.byref(degenerate), None, None, None, None, 0.9, 0.5,
                                            None, None, None, None, 0, None) == sp.SPARGE_EINVAL
     good = sp.make_shape(2, 4, 2, 1000, 128)
-    # status + V^T [B, Hkv, d, N_pad] bf16 + launch order of B*Hq*T_m int32 items + its scratch (256-B rounded)
+    # status + V^T [B, Hkv, N_pad/64, d, 64] bf16 + launch order of B*Hq*T_m int32 items + its scratch (256-B rounded)
     assert sp._lib.sparge_attn_workspace(ctypes.byref(good)) == 256 + 2 * 2 * 128 * 1024 * 2 + 256 + 512
     with pytest.raises(sp.SpargeError):
         sp.hilbert_permute(0, 4, 4)
