@@ -34,6 +34,8 @@ namespace {
 constexpr int kTile = 64;          // query blocks x key blocks per CTA
 #ifdef SPARGE_SHAT_8WARPS
 constexpr int kColSplit = 1;       // 8 warps, one 8-row strip x 64 keys each
+#elif defined(SPARGE_SHAT_COLSPLIT)
+constexpr int kColSplit = SPARGE_SHAT_COLSPLIT;
 #else
 constexpr int kColSplit = 2;       // 16 warps, one 8-row strip x 32 keys each
 #endif

@@ -284,3 +284,33 @@ def test_pipeline_batch2(lib, causal):
             _check_masks(gm[b, h], ref[h], f"batch {b} head {h}")
             assert rel_l1(og[b, h], ref[h]["o"]) < BUG_L1
             assert cnt[b, h, 0] == ref[h]["cnt"]["qk"]
+
+
+@pytest.mark.parametrize("N,d,Hkv,B,use_perm", [(1000, 128, 2, 1, False), (77, 64, 3, 2, True),
+                                                (4099, 128, 1, 1, True)])
+def test_v_staging_layout_bit_exact(lib, N, d, Hkv, B, use_perm):
+    """The V stage (k_vprep, SPARGE_ATTN_VPREP_ONLY) is pure data movement:
+    the workspace holds V^T tile-major [B, Hkv, N_pad/64, d, 64] with
+    V^T[b, h, r // 64, c, r % 64] = V[b, h, perm[r], c] and zeros for
+    r >= N (include/sparge.h, sparge_attn_workspace) -- compared bit for bit
+    with a numpy transform of the input."""
+    Hq = Hkv
+    rng = np.random.default_rng(N + d)
+    qn, kn, vn = (rng.standard_normal((B, Hq, N, d)).astype(np.float32) for _ in range(3))
+    q, k, v = _dev(qn), _dev(kn), _dev(vn)
+    perm = rng.permutation(N).astype(np.int32) if use_perm else None
+    pt = None if perm is None else torch.from_numpy(perm).cuda()
+    o, bf = lib.sparge_forward(q, k, v, 0.9, 0.5, -5.0, causal=False, perm=pt)
+    bf.workspace.zero_()
+    lib.sparge_attn_fwd_ex(bf.shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, -5.0, pt, o,
+                           None, bf.workspace, lib.SPARGE_ATTN_VPREP_ONLY)
+    torch.cuda.synchronize()
+    n_pad = (N + 63) // 64 * 64
+    vt = bf.workspace[256:256 + B * Hkv * d * n_pad * 2].view(torch.int16).cpu().numpy()
+    vt = vt.reshape(B, Hkv, n_pad // 64, d, 64)
+    src = v.view(torch.int16).cpu().numpy()                     # [B, Hkv, N, d] raw bf16 bits
+    rows = src if perm is None else src[:, :, perm, :]
+    want = np.zeros((B, Hkv, n_pad, d), np.int16)
+    want[:, :, :N] = rows
+    want = want.reshape(B, Hkv, n_pad // 64, 64, d).transpose(0, 1, 2, 4, 3)
+    assert np.array_equal(vt, want)
