@@ -274,7 +274,7 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
 
   // launch order: the longest items first, then groups of kv-heads whose
   // K^ + V^T fit the L2 budget, each longest first (k_order.cu)
-  static const int budget_mb = order_env("SPARGE_ORDER_BUDGET_MB", 48);
+  static const int budget_mb = order_env("SPARGE_ORDER_BUDGET_MB", 64);
   static const int n_long = order_env("SPARGE_ORDER_LONG", 296);
   const int64_t kv_head_bytes = static_cast<int64_t>(n_pad) * s.d * ((qk16 ? 2 : 1) + (pv8 ? 1 : 2));
   // groups of equal size: ceil(kv-heads / groups) kv-heads each
