@@ -115,7 +115,7 @@ def sample_dense_ops(cfg, qblocks):
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -135,6 +135,7 @@ class ClockSampler:
             time.sleep(0.2)
         except OSError:
             self.proc = None
+        self.t0 = time.time()          # the timed region starts now
         return self
 
     def _read(self):
@@ -142,6 +143,7 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.t1 = time.time()          # ... and ended (after the synchronize)
         if self.proc:
             time.sleep(0.1)
             self.proc.terminate()
@@ -153,20 +155,31 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        import datetime
+        outside = 0
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if not (self.t0 - 0.05 <= ts <= self.t1 + 0.05):   # one 50-ms sample of slack
+                    outside += 1
+                    continue
+            except (ValueError, AttributeError):
+                pass
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[3:7]):
+            for nm, val in zip(names, parts[4:8]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
-            return None
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "note": f"no 50-ms nvidia-smi sample fell inside the "
+                            f"{1e3 * (self.t1 - self.t0):.0f}-ms timed region ({outside} outside it)"}
         busy = [s for s in sm if s > 0.5 * max(sm)] or sm
         return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx),
                 "reasons": sorted(reasons), "samples": len(sm)}
