@@ -96,11 +96,12 @@ def dense_ops(cfg, B=1):
     return 4.0 * d * H * B * N * N
 
 
-def sample_qblocks(tm, seed=0):
+def sample_qblocks(tm, seed=0, n=8):
+    """The first, second, middle and last query blocks plus random ones, n in all."""
     rng = np.random.default_rng(seed)
-    base = {0, 1, tm // 2, tm - 1}
-    extra = rng.choice(tm, size=min(4, tm), replace=False).tolist()
-    return sorted(b for b in base.union(extra) if 0 <= b < tm)
+    base = {b for b in (0, 1, tm // 2, tm - 1) if 0 <= b < tm}
+    rest = [b for b in rng.permutation(tm).tolist() if b not in base]
+    return sorted(base.union(rest[:max(0, min(n, tm) - len(base))]))
 
 
 def sample_dense_ops(cfg, qblocks):
@@ -458,7 +459,9 @@ def cpu_leg(cfg, q, k, v, snap, perm_np):
     vs = v[0, 0].float().cpu().double().numpy()
     if perm_np is not None:
         qs, ks, vs = qs[perm_np], ks[perm_np], vs[perm_np]
-    qb = sample_qblocks(tm)
+    # ~10 s of oracle work on the GPU box's host: 128 query blocks at 32K
+    # (8.4 s measured for 96), scaled by 1/N
+    qb = sample_qblocks(tm, n=max(8, int(128 * 32768 / N)))
     t0 = time.perf_counter()
     o_ref, M, near, cnt, _ = O.spargeattn_head(qs, ks, vs, O.f32(cfg["tau"]), O.f32(cfg["theta"]),
                                                O.f32(cfg["lam"]), causal=cfg["causal"],
