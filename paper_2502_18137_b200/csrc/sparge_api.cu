@@ -273,8 +273,13 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
     return SPARGE_ECUDA;
 
   // launch order: the longest items first, then groups of kv-heads whose
-  // K^ + V^T fit the L2 budget, each longest first (k_order.cu)
-  static const int budget_mb = order_env("SPARGE_ORDER_BUDGET_MB", 64);
+  // K^ + V^T fit the L2 budget, each longest first (k_order.cu).  With the
+  // Hilbert permutation the kept blocks are local, so a CTA touches a small
+  // part of its head's K^/V^T and larger groups fit: 64 MB; in token order
+  // 48 MB (profiles/r01s6_quant_ab.txt).
+  static const int budget_perm_mb = order_env("SPARGE_ORDER_BUDGET_MB", 64);
+  static const int budget_plain_mb = order_env("SPARGE_ORDER_BUDGET_MB", 48);
+  const int budget_mb = perm ? budget_perm_mb : budget_plain_mb;
   static const int n_long = order_env("SPARGE_ORDER_LONG", 296);
   const int64_t kv_head_bytes = static_cast<int64_t>(n_pad) * s.d * ((qk16 ? 2 : 1) + (pv8 ? 1 : 2));
   // groups of equal size: ceil(kv-heads / groups) kv-heads each
