@@ -214,7 +214,9 @@ size_t sparge_attn_workspace(const sparge_shape* shape);
  *            P~V slice iff max_rows(m_local - m_new) > lambda (R5).
  *   perm     nullable int32 [N]: the same permutation given to
  *            sparge_quantize; V rows are gathered through it and O rows are
- *            scattered back to original order.
+ *            scattered back to original order.  Must be NULL when
+ *            shape->causal is set (causality is defined on token positions,
+ *            R8): SPARGE_EINVAL otherwise.
  *   o        [B, Hq, N, d] in_dtype, strided by o_str (written)
  *   counters nullable uint64 [B, Hq, 3], ACCUMULATED (caller zeroes):
  *            [0] executed QK tiles, [1] executed P~V warp slices,
@@ -256,6 +258,29 @@ int sparge_attn_fwd_ex(const sparge_shape* shape,
                        uint64_t* counters,
                        void* workspace, size_t ws_bytes, void* stream,
                        unsigned flags);
+
+/*
+ * sparge_attn_fwd_mpv -- sparge_attn_fwd plus a dump of every lambda-gate
+ * decision (debug mode of SURVEY §8(c); Algorithm 1 lines 14-17):
+ *   mpv  uint8 [B, Hq, T_m, T_n, c_w] device, caller-zeroed.  For every kept
+ *        block (i, j) and warp group w (rows 32w..32w+31 of query block i):
+ *        2 = the P~V slice was computed (max over the group's rows of
+ *        m_local - m_new > lambda), 1 = skipped by the gate (also a group
+ *        without valid rows, R6).  Entries of blocks that M_g drops stay 0.
+ * Same arguments, validation and errors as sparge_attn_fwd (mpv NULL ->
+ * SPARGE_EINVAL).  Writes one byte per (tile, warp): a test/debug entry
+ * point, not the timed path.
+ */
+int sparge_attn_fwd_mpv(const sparge_shape* shape,
+                        const void* qq, const float* dq,
+                        const void* kq, const float* dk,
+                        const void* v, sparge_strides v_str,
+                        const int32_t* lut, const int32_t* cnt,
+                        float lambda, const int32_t* perm,
+                        void* o, sparge_strides o_str,
+                        uint64_t* counters,
+                        void* workspace, size_t ws_bytes, void* stream,
+                        uint8_t* mpv);
 
 /*
  * sparge_l1_sums -- the accuracy metric of §3.6, relative L1

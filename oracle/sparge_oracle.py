@@ -35,6 +35,7 @@ __all__ = [
     "round_e4m3",
     "fp8_v_quant",
     "round_bf16",
+    "round_fp16",
     "sparse_attention",
     "dense_attention",
     "relative_l1",
@@ -325,6 +326,20 @@ def round_bf16(x):
     return np.ldexp(np.rint(m * 256.0) / 256.0, e)
 
 
+def round_fp16(x):
+    """Round fp64 values to the nearest IEEE binary16 value (11 significant
+    bits, normals from 2^-14, subnormals on the 2^-24 grid), ties to even,
+    directly from fp64 -- the P~ operand of the P~V product for fp16 inputs
+    (R12/R13: P~ is rounded to the input dtype).  P~ <= 1 here, so the
+    overflow range (> 65504) is not modelled."""
+    x = np.asarray(x, dtype=np.float64)
+    a = np.abs(x)
+    _, e = np.frexp(a)                   # a = m 2^e, 0.5 <= m < 1
+    E = np.maximum(e - 1, -14)           # exponent of the leading bit; subnormals share -14
+    q = np.ldexp(1.0, E - 10)            # spacing of representable values around a
+    return np.copysign(np.rint(a / q) * q, x)
+
+
 E4M3_MAX = 448.0
 
 
@@ -361,7 +376,7 @@ def fp8_v_quant(V):
 # Alg. 1 lines 7-21: stage 2, the sparse FlashAttention loop.
 # --------------------------------------------------------------------------
 def sparse_attention(Q, K, V, M, lam, bq=128, bk=64, cw=4, causal=False, quant=None,
-                     pv_round="bf16", qblocks=None, v_fp8=None):
+                     pv_round="bf16", qblocks=None, v_fp8=None, trace=False):
     """O for one head, following Algorithm 1 and the online
     softmax of Eq. (1).
 
@@ -370,9 +385,15 @@ def sparse_attention(Q, K, V, M, lam, bq=128, bk=64, cw=4, causal=False, quant=N
             / sqrt(d) (line 12; 1/sqrt(d) per R3) -- the integer
             product is exact;
     V: fp64 [N, d];  M: [T_m, T_n] mask (line 10);  lam: lambda (natural-log
-    units of S, R3; -inf disables);  pv_round: "bf16" rounds P~ before P~V
-    (R12/R13), None keeps fp64, "fp8" is the f4 product (R27): e4m3(128 P~)
-    times V^ of v_fp8 = fp8_v_quant(V), O = acc * s / (128 l).
+    units of S, R3; -inf disables);  pv_round: "bf16" / "fp16" round P~ to the
+    input dtype before P~V (R12/R13), None keeps fp64, "fp8" is the f4
+    product (R27): e4m3(128 P~) times V^ of v_fp8 = fp8_v_quant(V),
+    O = acc * s / (128 l).
+    trace: also record every gate decision of line 15 -- counters gain
+    "mpv" uint8 [T_m, T_n, cw] (2 computed, 1 skipped, 0 block not kept),
+    "gap" fp64 [T_m, T_n, cw] (g = max over the group's rows of
+    m_local - m_new; NaN where not kept) and "mag" fp64 [T_m, T_n, cw]
+    (max |m_local|, |m_new| over the group: the scale of S there).
     qblocks: optional list of q-block indices to compute (sampling); other
     rows of O are NaN.
 
@@ -391,6 +412,10 @@ def sparse_attention(Q, K, V, M, lam, bq=128, bk=64, cw=4, causal=False, quant=N
         K = np.asarray(K, dtype=np.float64)
     O = np.full((n, d), np.nan)
     cnt = dict(qk=0, pv_slices=0)
+    if trace:
+        cnt["mpv"] = np.zeros((tm, tn, cw), dtype=np.uint8)
+        cnt["gap"] = np.full((tm, tn, cw), np.nan)
+        cnt["mag"] = np.full((tm, tn, cw), np.nan)
     wrows = bq // cw
     for i in (range(tm) if qblocks is None else qblocks):
         r0, r1 = i * bq, min((i + 1) * bq, n)
@@ -427,12 +452,19 @@ def sparse_attention(Q, K, V, M, lam, bq=128, bk=64, cw=4, causal=False, quant=N
                 if a >= b:
                     continue                    # warp with no valid rows (R6)
                 g = np.max(gap[a:b])
+                if trace:
+                    cnt["mpv"][i, j, w] = 2 if g > lam else 1
+                    cnt["gap"][i, j, w] = g
+                    fin = np.concatenate([m_loc[a:b], m_new[a:b]])
+                    fin = fin[np.isfinite(fin)]
+                    cnt["mag"][i, j, w] = np.max(np.abs(fin)) if fin.size else 0.0
                 if g > lam:                     # compute iff > lambda (R5)
                     if pv_round == "fp8":
                         Pw = round_e4m3(P[a:b] * 128.0)
                         Oi[a:b] = alpha[a:b, None] * Oi[a:b] + Pw @ v_fp8[0][c0:c1]
                     else:
-                        Pw = round_bf16(P[a:b]) if pv_round == "bf16" else P[a:b]
+                        rnd = {"bf16": round_bf16, "fp16": round_fp16, None: None}[pv_round]
+                        Pw = rnd(P[a:b]) if rnd is not None else P[a:b]
                         Oi[a:b] = alpha[a:b, None] * Oi[a:b] + Pw @ V[c0:c1]
                     cnt["pv_slices"] += 1
             m = m_new
@@ -482,7 +514,7 @@ def sparsity_of(qk_exec, pv_slices_exec, live_tiles, cw=4):
 
 def spargeattn_head(q, k, v, tau, theta, lam, bq=128, bk=64, cw=4, causal=False,
                     sim_mode="cosine", quantize=True, pv_round="bf16", qblocks=None,
-                    smooth=False):
+                    smooth=False, trace=False):
     """The whole of Algorithm 1 for one head: stage 1 (lines 3-6) then the
     sparse loop (lines 7-21).  smooth: K smoothing before the INT8
     quantisation (row f4, R28; stage 1 keeps the raw K, R14) -- True (mu of
@@ -503,5 +535,5 @@ def spargeattn_head(q, k, v, tau, theta, lam, bq=128, bk=64, cw=4, causal=False,
         quant = (Qq, dq, Kq, dk)
     v_fp8 = fp8_v_quant(v) if pv_round == "fp8" else None
     O, cnt = sparse_attention(q, k, v, M, lam, bq, bk, cw, causal, quant, pv_round, qblocks,
-                              v_fp8)
+                              v_fp8, trace)
     return O, M, near, cnt, quant

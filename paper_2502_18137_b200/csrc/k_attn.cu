@@ -157,6 +157,7 @@ struct Smem {
   static constexpr int OFF_MISC = (OFF_BAR + N_BARS * 8 + 15) / 16 * 16;
   static constexpr int TOTAL = OFF_MISC + 16 + 16 * NSB;
   static constexpr int BYTES = (TOTAL + 1023) / 1024 * 1024;
+  static_assert(VST >= NSB, "the V-slot release waits on QK(t - VST + NSB) <= QK(t)");
   // INT8: one K-atom of D bytes per row (128 -> SW128, 64 -> SW64); 16-bit:
   // 128-B atoms, the second (d = 128) BQ*128 / BK*128 bytes after the first
   static constexpr int ROW_BYTES_QK = QK16 ? 128 : D;
@@ -176,6 +177,7 @@ struct AttnParams {
   unsigned int* status;
   const float* v_scale;   // PV8: per-(b, hkv, channel) dequant scale s_c [B*Hkv, D]
   const int32_t* order;   // work items (bhq * T_m + i), the launch order of k_order
+  uint8_t* mpv;           // debug: M_pv decisions [B*Hq*T_m, T_n, 4] (nullptr = off)
   float lam2;         // lambda * log2(e)
   float scale_log2;   // log2(e) / sqrt(d)
   int N, T_m, T_n, Hq, Hkv, group;
@@ -416,10 +418,12 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         }
         const int vs = t % VST;
         // V slot of tile t - VST is free once P~V(t - VST) is done, i.e. once
-        // QK(t - VST + 2) -- issued after it -- is (its s_full commit covers
-        // every earlier MMA; a skipped P~V needs nothing)
+        // QK(t - VST + NSB) -- the next QK issued after it (issue order:
+        // QK(u + NSB - 1), P~V(u), QK(u + NSB)) -- is (its s_full commit
+        // covers every earlier MMA; a skipped P~V needs nothing).  u <= t
+        // because VST >= NSB, so that QK's K tile is already in flight.
         if (t >= VST) {
-          const int u = t - VST + 2;
+          const int u = t - VST + L::NSB;
           mbar_wait(s_full + u % KST, (u / KST) & 1);
         }
         mbar_arrive_expect_tx(v_full + vs, L::V_BYTES);
@@ -631,6 +635,10 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         const float m_new = fmaxf(m_true, m_loc);
         // Alg. 1 line 15: max_{r in I_w}(m_local - m_new) > lambda, as a vote
         compute = __any_sync(0xffffffffu, row_has && (m_loc - m_new > p.lam2));
+        // debug dump of the gate decision of (tile j, warp quad): 2 = P~V
+        // computed, 1 = skipped by the lambda gate (0 stays: block not kept)
+        if (p.mpv != nullptr && lane == 0)
+          p.mpv[(row_id * p.T_n + j) * NSOFT + quad] = compute ? 2 : 1;
         // lazy rescale (R22): move the reference max only when it lags the
         // true max by more than the threshold (always when it is -inf)
         need = compute && (m_new > m_ref + kRefThreshold);
@@ -773,8 +781,9 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
                         const int32_t* lut, const int32_t* cnt, float lambda,
                         const int32_t* perm, void* o, sparge_strides o_str,
                         uint64_t* counters, unsigned int* status, const float* v_scale,
-                        const int32_t* order, cudaStream_t stream) {
+                        const int32_t* order, uint8_t* mpv, cudaStream_t stream) {
   AttnParams p;
+  p.mpv = mpv;
   p.v_scale = v_scale;
   p.order = order;
   p.dq = dq; p.dk = dk; p.lut = lut; p.cnt = cnt; p.perm = perm;

@@ -205,11 +205,13 @@ int sparge_attn_fwd(const sparge_shape* shape, const void* qq, const float* dq,
                             counters, workspace, ws_bytes, stream, 0u);
 }
 
-int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* dq,
-                       const void* kq, const float* dk, const void* v, sparge_strides v_str,
-                       const int32_t* lut, const int32_t* cnt, float lambda,
-                       const int32_t* perm, void* o, sparge_strides o_str, uint64_t* counters,
-                       void* workspace, size_t ws_bytes, void* stream, unsigned flags) {
+namespace {
+int attn_fwd_impl(const sparge_shape* shape, const void* qq, const float* dq,
+                  const void* kq, const float* dk, const void* v, sparge_strides v_str,
+                  const int32_t* lut, const int32_t* cnt, float lambda,
+                  const int32_t* perm, void* o, sparge_strides o_str, uint64_t* counters,
+                  void* workspace, size_t ws_bytes, void* stream, unsigned flags,
+                  uint8_t* mpv) {
   if (flags > 2u) return SPARGE_EINVAL;
   if (!shape_ok(shape) || !qq || !dq || !kq || !dk || !v || !lut || !cnt || !o || !workspace)
     return SPARGE_EINVAL;
@@ -219,6 +221,9 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
   if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return SPARGE_EINVAL;
   if (ws_bytes < sparge_attn_workspace(shape)) return SPARGE_EINVAL;
   if (!(lambda < 0.f)) return SPARGE_EINVAL;   // lambda < 0 or -inf (§3.6)
+  // causal masking is defined on token positions (R8); with a permutation the
+  // kernel would apply it to permuted positions, which is not causal attention
+  if (shape->causal && perm) return SPARGE_EINVAL;
   const bool pv8 = shape->pv_dtype == SPARGE_PV_FP8_E4M3;
   if (pv8 && shape->qk_dtype != SPARGE_QK_INT8) return SPARGE_ENOTIMPL;   // FP8 PV with INT8 QK only
   if (shape->smooth_k && shape->qk_dtype != SPARGE_QK_INT8) return SPARGE_ENOTIMPL;
@@ -293,8 +298,28 @@ int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* d
                    n_long, order, order + round256(static_cast<size_t>(n_it) * 4) / 4, st);
   if (e != cudaSuccess) return SPARGE_ECUDA;
   e = launch_attn(s, mq, mk, mv, dq, dk, lut, cnt, lambda, perm, o, o_str, counters, status,
-                  pv8 ? v_scale : nullptr, order, st);
+                  pv8 ? v_scale : nullptr, order, mpv, st);
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
+}
+}  // namespace
+
+int sparge_attn_fwd_ex(const sparge_shape* shape, const void* qq, const float* dq,
+                       const void* kq, const float* dk, const void* v, sparge_strides v_str,
+                       const int32_t* lut, const int32_t* cnt, float lambda,
+                       const int32_t* perm, void* o, sparge_strides o_str, uint64_t* counters,
+                       void* workspace, size_t ws_bytes, void* stream, unsigned flags) {
+  return attn_fwd_impl(shape, qq, dq, kq, dk, v, v_str, lut, cnt, lambda, perm, o, o_str,
+                       counters, workspace, ws_bytes, stream, flags, nullptr);
+}
+
+int sparge_attn_fwd_mpv(const sparge_shape* shape, const void* qq, const float* dq,
+                        const void* kq, const float* dk, const void* v, sparge_strides v_str,
+                        const int32_t* lut, const int32_t* cnt, float lambda,
+                        const int32_t* perm, void* o, sparge_strides o_str, uint64_t* counters,
+                        void* workspace, size_t ws_bytes, void* stream, uint8_t* mpv) {
+  if (!mpv) return SPARGE_EINVAL;
+  return attn_fwd_impl(shape, qq, dq, kq, dk, v, v_str, lut, cnt, lambda, perm, o, o_str,
+                       counters, workspace, ws_bytes, stream, 0u, mpv);
 }
 
 int sparge_l1_sums(const void* o, const void* o_ref, int dtype, int64_t n, double* out,

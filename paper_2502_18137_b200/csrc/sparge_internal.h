@@ -49,7 +49,7 @@ cudaError_t launch_attn(const sparge_shape& s, const CUtensorMap& mq, const CUte
                         const int32_t* lut, const int32_t* cnt, float lambda,
                         const int32_t* perm, void* o, sparge_strides o_str,
                         uint64_t* counters, unsigned int* status, const float* v_scale,
-                        const int32_t* order, cudaStream_t stream);
+                        const int32_t* order, uint8_t* mpv, cudaStream_t stream);
 
 int attn_smem_bytes(int d, int qk16);
 

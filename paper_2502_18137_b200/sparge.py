@@ -69,6 +69,8 @@ _lib.sparge_attn_fwd.argtypes = [ctypes.POINTER(Shape), _vp, _vp, _vp, _vp, _vp,
                                  ctypes.c_size_t, _vp]
 _lib.sparge_attn_fwd_ex.restype = ctypes.c_int
 _lib.sparge_attn_fwd_ex.argtypes = _lib.sparge_attn_fwd.argtypes + [ctypes.c_uint]
+_lib.sparge_attn_fwd_mpv.restype = ctypes.c_int
+_lib.sparge_attn_fwd_mpv.argtypes = _lib.sparge_attn_fwd.argtypes + [_vp]
 _lib.sparge_l1_sums.restype = ctypes.c_int
 _lib.sparge_l1_sums.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int64, _vp, _vp]
 SPARGE_L1_OUT_DOUBLES = 1186
@@ -85,7 +87,7 @@ _lib.sparge_quantize_smooth_k.argtypes = [ctypes.POINTER(Shape), _vp, Strides, _
 
 EXPORTED = ("sparge_strerror", "hilbert_permute", "sparge_quantize", "sparge_predict_mask",
             "sparge_predict_workspace",
-            "sparge_attn_workspace", "sparge_attn_fwd", "sparge_attn_fwd_ex",
+            "sparge_attn_workspace", "sparge_attn_fwd", "sparge_attn_fwd_ex", "sparge_attn_fwd_mpv",
             "sparge_attn_status", "sparge_l1_sums", "sparge_smooth_k_workspace",
             "sparge_smooth_k_mean", "sparge_quantize_smooth_k")
 SPARGE_ATTN_VPREP_ONLY, SPARGE_ATTN_SKIP_VPREP = 1, 2
@@ -187,6 +189,17 @@ def sparge_attn_fwd_ex(shape, qq, dq, kq, dk, v, lut, cnt, lam, perm, o, counter
         int(flags)))
 
 
+def sparge_attn_fwd_mpv(shape, qq, dq, kq, dk, v, lut, cnt, lam, perm, o, counters, workspace,
+                        mpv, stream=None):
+    """sparge_attn_fwd plus the lambda-gate decision dump mpv uint8
+    [B, Hq, T_m, T_n, 4] (caller-zeroed; 2 computed, 1 skipped, 0 not kept)."""
+    _check("sparge_attn_fwd_mpv", _lib.sparge_attn_fwd_mpv(
+        ctypes.byref(shape), _ptr(qq), _ptr(dq), _ptr(kq), _ptr(dk), _ptr(v), _strides(v),
+        _ptr(lut), _ptr(cnt), float(lam), _ptr(perm), _ptr(o), _strides(o), _ptr(counters),
+        _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream),
+        _ptr(mpv)))
+
+
 def sparge_l1_sums(o, o_ref, out=None, stream=None):
     """Device relative-L1 sums of two same-shape contiguous bf16/fp16 tensors
     (§3.6).  Returns the device fp64 buffer; out[0] = sum|o - o_ref|,
@@ -250,22 +263,65 @@ class Buffers:
             self.k_mean = torch.empty(B, Hkv, d, dtype=torch.float32, **kw)
 
 
+def _same_shape(a, b):
+    return all(getattr(a, f) == getattr(b, f) for f, _ in Shape._fields_)
+
+
+def _validate(q, k, v, out, perm, causal):
+    """Reject what the C ABI cannot see: dtypes, devices and shape agreement
+    (the library gets raw pointers and would read e.g. fp32 bytes as bf16)."""
+    ts = [("q", q), ("k", k), ("v", v)] + ([("out", out)] if out is not None else [])
+    for name, t in ts:
+        if not isinstance(t, torch.Tensor) or t.dim() != 4:
+            raise ValueError(f"{name} must be a 4-D torch tensor [B, H, N, d]")
+        if t.dtype not in (torch.bfloat16, torch.float16):
+            raise ValueError(f"{name} must be bf16 or fp16, got {t.dtype}")
+        if t.dtype != q.dtype or t.device != q.device:
+            raise ValueError(f"{name} must have q's dtype and device")
+    B, Hq, N, d = q.shape
+    if k.shape != v.shape or k.shape[0] != B or k.shape[2] != N or k.shape[3] != d:
+        raise ValueError(f"k/v must be [B, Hkv, N, d] = [{B}, Hkv, {N}, {d}]; got "
+                         f"{tuple(k.shape)} / {tuple(v.shape)}")
+    if Hq % k.shape[1]:
+        raise ValueError("Hq must be a multiple of Hkv (GQA)")
+    if out is not None and out.shape != q.shape:
+        raise ValueError("out must have q's shape")
+    if q.device.type != "cuda":
+        raise ValueError("q, k, v must be CUDA tensors (there is no CPU path)")
+    if perm is not None:
+        if perm.dtype != torch.int32 or perm.device != q.device or perm.numel() != N:
+            raise ValueError("perm must be an int32 tensor of N elements on q's device")
+        if causal:
+            raise ValueError("causal attention with a token permutation is undefined (R8)")
+
+
 def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=None, out=None,
                    sim_mode=SPARGE_SIM_COSINE, stream=None, qk_dtype=SPARGE_QK_INT8,
-                   pv_dtype=SPARGE_PV_SAME_AS_INPUT, smooth_k=False):
+                   pv_dtype=SPARGE_PV_SAME_AS_INPUT, smooth_k=False, counters=None, mpv=None):
     """The whole hot path (a1 quantise Q, K -> a2 predict -> a3 attention) on
     device tensors q [B,Hq,N,d], k/v [B,Hkv,N,d] (bf16 or fp16).  perm: optional
     int32 device tensor [N] (Hilbert order); O is returned in original order.
     qk_dtype=SPARGE_QK_INPUT selects the unquantised "SpargeAttn+FA2" kernel;
     pv_dtype=SPARGE_PV_FP8_E4M3 the FP8 P~V product and smooth_k=True the K
     smoothing (row f4, R28).
+    counters: None -> buffers.counters, zeroed first (the C ABI accumulates);
+    False -> not counted.  mpv: optional caller-zeroed uint8 [B,Hq,T_m,T_n,4]
+    device tensor that receives the lambda-gate decisions (debug mode).
     Returns (O, buffers)."""
+    _validate(q, k, v, out, perm, causal)
     B, Hq, N, d = q.shape
     Hkv = k.shape[1]
     shape = make_shape(B, Hq, Hkv, N, d, causal, q.dtype, sim_mode, qk_dtype, pv_dtype, smooth_k)
     if buffers is None:
         buffers = Buffers(shape, device=q.device)
+    elif not _same_shape(buffers.shape, shape):
+        raise ValueError("buffers were allocated for a different shape / mode")
     bf = buffers
+    if counters is None:
+        counters = bf.counters
+        counters.zero_()
+    elif counters is False:
+        counters = None
     o = torch.empty_like(q) if out is None else out
     sparge_quantize(shape, q, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim, stream)
     if smooth_k:
@@ -276,8 +332,12 @@ def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=No
         sparge_quantize(shape, k, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim, stream)
     sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, tau, theta,
                         bf.mask, bf.lut, bf.cnt, bf.pred_workspace, stream)
-    sparge_attn_fwd(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm, o,
-                    bf.counters, bf.workspace, stream)
+    if mpv is not None:
+        sparge_attn_fwd_mpv(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm, o,
+                            counters, bf.workspace, mpv, stream)
+    else:
+        sparge_attn_fwd(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm, o,
+                        counters, bf.workspace, stream)
     return o, bf
 
 
@@ -335,7 +395,7 @@ class HostPipeline:
                 sparge_forward(self.q[:, qs], self.k[:, ks], self.v[:, ks], tau, theta, lam,
                                causal=bool(self.shape.causal), perm=perm, buffers=bf,
                                out=self.o[:, qs], stream=self.s_comp,
-                               qk_dtype=self.shape.qk_dtype)
+                               qk_dtype=self.shape.qk_dtype, counters=False)
                 ev_out = torch.cuda.Event()
                 ev_out.record(self.s_comp)
             with torch.cuda.stream(self.s_d2h):

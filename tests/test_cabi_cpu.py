@@ -65,3 +65,38 @@ def test_hilbert_matches_oracle(sp, T, H, W, pre):
     perm, inv = sp.hilbert_permute(T, H, W, pre)
     p_ref, i_ref = O.hilbert_permutation(T, H, W, pre)
     assert np.array_equal(perm, p_ref) and np.array_equal(inv, i_ref)
+
+
+def test_causal_with_permutation_rejected_by_abi(sp):
+    """causal masking is defined on token positions (R8), so the C
+    ABI refuses a permutation together with causal=1 before touching memory."""
+    shape = sp.make_shape(1, 1, 1, 256, 128, causal=True)
+    st = sp.Strides(0, 256 * 128, 128)
+    fake = ctypes.c_void_p(1 << 20)          # never dereferenced: validation fails first
+    ws = sp._lib.sparge_attn_workspace(ctypes.byref(shape))
+    rc = sp._lib.sparge_attn_fwd(ctypes.byref(shape), fake, fake, fake, fake, fake, st, fake,
+                                 fake, -5.0, fake, fake, st, None, fake, ws, None)
+    assert rc == sp.SPARGE_EINVAL
+    rc = sp._lib.sparge_attn_fwd_mpv(ctypes.byref(shape), fake, fake, fake, fake, fake, st, fake,
+                                     fake, -5.0, None, fake, st, None, fake, ws, None, None)
+    assert rc == sp.SPARGE_EINVAL            # mpv NULL
+
+
+def test_python_binding_validates_inputs(sp):
+    """the binding rejects what raw pointers cannot carry (dtype,
+    device, shape agreement) instead of handing wrong bytes to the kernels."""
+    import torch
+    q = torch.zeros(1, 2, 256, 64, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="CUDA"):
+        sp.sparge_forward(q, q[:, :1], q[:, :1], 0.9, 0.5, -5.0)
+    with pytest.raises(ValueError, match="bf16 or fp16"):
+        sp._validate(q.float(), q, q, None, None, False)
+    with pytest.raises(ValueError, match="q's dtype"):
+        sp._validate(q, q.half(), q, None, None, False)
+    with pytest.raises(ValueError, match="Hkv"):
+        sp._validate(q, q[:, :1, :128], q[:, :1, :128], None, None, False)
+    q4 = torch.zeros(1, 4, 256, 64, dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="multiple of Hkv"):
+        sp._validate(q4, q4[:, :3], q4[:, :3], None, None, False)
+    with pytest.raises(ValueError, match="out"):
+        sp._validate(q4, q4[:, :2], q4[:, :2], q4[:, :1], None, False)

@@ -7,7 +7,7 @@ import pytest
 import torch
 
 import oracle as O
-from helpers import bf16_np, oracle_forward, rel_l1
+from helpers import check_o, bf16_np, oracle_forward, rel_l1
 from paper_2502_18137_b200 import inputs
 
 pytestmark = pytest.mark.gpu
@@ -85,5 +85,4 @@ def test_pipeline_with_smoothing(lib, N, Hq, Hkv, causal):
                          causal=causal, group=Hq // Hkv, smooth=True)
     og = bf16_np(o_s)[0]
     for h in range(Hq):
-        err = rel_l1(og[h], ref[h]["o"])
-        assert err < BUG_L1, (h, err)
+        err, _ = check_o(og[h], ref[h]["o"])

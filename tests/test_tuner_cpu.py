@@ -87,7 +87,7 @@ def test_tune_layer_with_the_oracle_as_evaluator():
         errs, sps = [], []
         for q, k, v, ref in cal:
             o, M, near, cnt, _ = O.spargeattn_head(q, k, v, O.f32(tau), O.f32(theta), O.f32(lam),
-                                                   pv_round="none")
+                                                   pv_round=None)
             errs.append(O.relative_l1(o, ref))
             sps.append(O.sparsity_of(cnt["qk"], cnt["pv_slices"], M.size))
         return max(errs), float(np.mean(sps))
