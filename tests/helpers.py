@@ -52,6 +52,11 @@ def rel_l1(a, b):
 
 HEAD_L1 = 5e-3     # whole-head relative L1 vs the oracle: the bug signal (north star: 2e-2)
 ROW_L1 = 2e-2      # every single query row must also be within the north star's 2e-2
+# FP8 P~V (row f4, R27): a P~ entry within rounding reach of an E4M3 midpoint
+# may round to the other neighbour on the GPU (fp32 exp2) than in the fp64
+# oracle -- one E4M3 step is 2^-3 relative, so one such flip on a row's
+# dominant key moves that row by up to 2^-3 (R30).  Head L1 stays 5e-3.
+ROW_L1_FP8 = 2.0 ** -3
 
 
 def check_o(o, o_ref, label="", head_tol=HEAD_L1, row_tol=ROW_L1):

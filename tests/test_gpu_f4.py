@@ -16,7 +16,7 @@ import pytest
 import torch
 
 import oracle as O
-from helpers import check_o, bf16_np, oracle_forward, rel_l1
+from helpers import ROW_L1_FP8, check_o, bf16_np, oracle_forward, rel_l1
 from paper_2502_18137_b200 import inputs
 
 pytestmark = pytest.mark.gpu
@@ -72,7 +72,7 @@ def test_c1_planted_fp8(lib):
     ref = oracle_forward(bf16_np(q)[0], bf16_np(k)[0], bf16_np(v)[0], 0.9, 0.5, -5.0,
                          pv_round="fp8")[0]
     _check_masks(bf.mask.cpu().numpy()[0, 0], ref, "C1")
-    err, _ = check_o(bf16_np(o)[0, 0], ref["o"])
+    err, _ = check_o(bf16_np(o)[0, 0], ref["o"], row_tol=ROW_L1_FP8)
     cnt = bf.counters.cpu().numpy()[0, 0]
     assert cnt[0] == ref["cnt"]["qk"]
     # PV slices: exact per decision in tests/test_gpu_mpv.py
@@ -94,7 +94,7 @@ def test_fp8_ragged(lib, N, d, Hq, Hkv, causal, dtype):
     cnt = bf.counters.cpu().numpy()[0]
     for h in range(Hq):
         _check_masks(gm[h], ref[h], f"head {h}")
-        err, _ = check_o(og[h], ref[h]["o"])
+        err, _ = check_o(og[h], ref[h]["o"], row_tol=ROW_L1_FP8)
         assert cnt[h, 0] == ref[h]["cnt"]["qk"]
 
 
@@ -109,7 +109,7 @@ def test_fp8_hilbert_and_filters_off(lib):
                              perm=perm.astype(np.int64), pv_round="fp8")
         for h in range(2):
             _check_masks(bf.mask.cpu().numpy()[0][h], ref[h], f"head {h}")
-            check_o(bf16_np(o)[0, h], ref[h]["o"], "test_gpu_f4")
+            check_o(bf16_np(o)[0, h], ref[h]["o"], "test_gpu_f4", row_tol=ROW_L1_FP8)
 
 
 def test_fp8_with_qk_input_is_not_implemented(lib):

@@ -54,37 +54,34 @@ def _free_port():
 
 
 def _worker(rank, world, port, q, k, v, out_path):
+    """One rank of the head-sharded run, through the product's plumbing
+    (paper_2502_18137_b200.multigpu): its heads, its compute (here the
+    oracle: the kernels need a B200), the all-gather of O and the
+    max-over-ranks timing reduction."""
     import oracle as O
+    from paper_2502_18137_b200 import multigpu
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     Hq, Hkv = q.shape[0], k.shape[0]
-    q0, q1, kv0, kv1 = shard_heads(Hq, Hkv, world, rank)
+    hq, hkv = multigpu.local_heads(Hq, Hkv)
     group = Hq // Hkv
+    assert all(h // group in hkv for h in hq)
     mine = np.stack([O.spargeattn_head(q[h], k[h // group], v[h // group], 0.9, 0.5, -5.0,
-                                       causal=True)[0] for h in range(q0, q1)])
-    t = torch.from_numpy(mine)
-    sizes = [shard_heads(Hq, Hkv, world, r)[1] - shard_heads(Hq, Hkv, world, r)[0]
-             for r in range(world)]
-    bufs = [torch.empty((s,) + tuple(t.shape[1:]), dtype=t.dtype) for s in sizes]
-    # gloo all_gather needs equal shapes: pad to the largest shard
-    mx = max(sizes)
-    pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype)
-    pad[: t.shape[0]] = t
-    gathered = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(gathered, pad)
-    # the max-over-ranks timing reduction bench.py uses
-    tm = torch.tensor([float(rank + 1)], dtype=torch.float64)
-    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+                                       causal=True)[0] for h in hq]) if hq else \
+        np.zeros((0,) + q.shape[1:])
+    full = multigpu.gather_heads(torch.from_numpy(mine)[None], Hq, Hkv)[0]
+    tm = multigpu.max_over_ranks(float(rank + 1))
+    assert tm == world
     if rank == 0:
-        full = torch.cat([g[:s] for g, s in zip(gathered, sizes)]).numpy()
-        np.save(out_path, full)
-        assert tm.item() == world
+        np.save(out_path, full.numpy())
     dist.destroy_process_group()
 
 
-def test_head_sharded_gather_equals_single_process(tmp_path):
+@pytest.mark.parametrize("Hq,Hkv", [(4, 2), (6, 3), (2, 2)])
+def test_head_sharded_gather_equals_single_process(tmp_path, Hq, Hkv):
+    """Uneven shards too: 3 kv-groups over 2 ranks -> 2 + 1."""
     g = np.random.default_rng(0)
-    Hq, Hkv, N, d = 4, 2, 300, 32
+    N, d = 300, 32
     q = g.standard_normal((Hq, N, d))
     k = g.standard_normal((Hkv, N, d))
     v = g.standard_normal((Hkv, N, d))
@@ -92,6 +89,7 @@ def test_head_sharded_gather_equals_single_process(tmp_path):
     mp.spawn(_worker, args=(2, _free_port(), q, k, v, out), nprocs=2, join=True)
     got = np.load(out)
     import oracle as O
-    ref = np.stack([O.spargeattn_head(q[h], k[h // 2], v[h // 2], 0.9, 0.5, -5.0,
+    grp = Hq // Hkv
+    ref = np.stack([O.spargeattn_head(q[h], k[h // grp], v[h // grp], 0.9, 0.5, -5.0,
                                       causal=True)[0] for h in range(Hq)])
     assert np.array_equal(got, ref)
