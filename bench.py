@@ -70,9 +70,9 @@ def gen_inputs(cfg, seed, heads=None):
     """float32 numpy [1, H, N, d] arrays + optional Hilbert perm (numpy int32)."""
     from paper_2502_18137_b200 import inputs
     perm = None
-    if cfg["kind"] == "llm_local":
-        q, k, v = inputs.llm_local(seed, cfg["N"], d=cfg["d"], Hq=cfg["Hq"], Hkv=cfg["Hkv"],
-                                   heads=heads)
+    if cfg["kind"] in ("llm_local", "llm_rope"):
+        gen = inputs.llm_rope if cfg["kind"] == "llm_rope" else inputs.llm_local
+        q, k, v = gen(seed, cfg["N"], d=cfg["d"], Hq=cfg["Hq"], Hkv=cfg["Hkv"], heads=heads)
     elif cfg["kind"] == "video":
         q, k, v = inputs.video(seed, cfg["T"], cfg["H"], cfg["W"], d=cfg["d"], heads=cfg["Hq"],
                                text_prefix=cfg["text_prefix"], heads_subset=heads)

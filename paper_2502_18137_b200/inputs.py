@@ -11,10 +11,20 @@ Recipes (the structure each one plants and why):
                with one non-self-similar Q block (i=5) and K block (j=11)
                that are i.i.d. (CosSim ~1/n < theta) -- exercises TopCdf and
                both forcing rules of Eq. 5.
-  llm_local    C2/C5: per kv-head AR(1) latent z_t (rho = 0.998, lag-64
-               correlation ~0.88) projected per head, plus noise; q-heads of
-               a GQA group share the latent; token 0 is an attention sink.
-               Produces local + sink attention, the Llama pattern of Fig. 2.
+  llm_rope     C2/C5 (round 2): Llama-style rotary position embedding
+               (base 500000, rotate-half pairs) on per-head content vectors
+               that share a kv-group direction, plus a slowly drifting AR(1)
+               latent and a little noise.  With geometric RoPE frequencies
+               q_t . k_s decays like -beta ln|t - s| (the long-term decay of
+               RoPE), i.e. a power-law attention profile; token 0 is a sink
+               key living in the lowest-frequency pairs (position-independent
+               logit); V carries a shared per-head mean direction (as real
+               value vectors do).  Tuned (scripts/tune_gen_rope.py, oracle
+               only) so that at the paper's l1 = 0.08 the reachable sparsity
+               RISES with N, the direction of Table 8.
+  llm_local    round-1 C2/C5 generator (kept for the small parity cases):
+               per kv-head AR(1) latent z_t (rho = 0.998) projected per head,
+               plus noise; token 0 is an attention sink.
   video        C3/C4: a sum of 8 random low-frequency cosines over (t, h, w)
                projected per head, plus noise; an optional i.i.d. text
                prefix.  Smooth neighbouring tokens (Fig. 4) so the Hilbert
@@ -26,7 +36,7 @@ import math
 
 import numpy as np
 
-__all__ = ["planted", "llm_local", "video", "gaussian", "to_device", "WORKLOADS"]
+__all__ = ["planted", "llm_local", "llm_rope", "video", "gaussian", "to_device", "WORKLOADS"]
 
 
 def _rng(seed):
@@ -105,6 +115,68 @@ def llm_local(seed, N, d=128, Hq=32, Hkv=8, B=1, gamma=0.7, noise=0.6, rho=0.998
     return q, k, v
 
 
+def rope(x, base=500000.0, pos=None):
+    """Rotary position embedding of rows x [N, d] at positions 0..N-1 (the
+    Llama rotate-half convention: pair (c, c + d/2) rotated by t * w_c,
+    w_c = base^(-2c/d)).  Input synthesis only -- the method under test never
+    sees positions."""
+    n, d = x.shape
+    h = d // 2
+    w = base ** (-np.arange(h) * 2.0 / d)
+    ang = (np.arange(n, dtype=np.float64) if pos is None else pos)[:, None] * w[None, :]
+    c, s_ = np.cos(ang), np.sin(ang)
+    x1, x2 = x[:, :h], x[:, h:]
+    return np.concatenate([x1 * c - x2 * s_, x1 * s_ + x2 * c], 1)
+
+
+def llm_rope(seed, N, d=128, Hq=32, Hkv=8, B=1, gamma=0.9, alpha=0.05, noise=0.05, rho=0.998,
+             head_jitter=0.3, sink=0.85, sink_pairs=8, vmean=1.0, v_noise=0.5, base=500000.0,
+             heads=None):
+    """C2 / C5.  Per kv-head g: content c ~ N(0, I_d), AR(1)
+    latent z; K_s = gamma RoPE_s(c + e_k + alpha z_s W_k + noise);
+    per q-head h of the group Q_t = gamma RoPE_t(c + e_h + alpha z_t W_q,h +
+    noise) (e_k, e_h: head jitter); key 0 is a sink whose logit against every
+    query is ~sink x the diagonal logit (its energy sits in the `sink_pairs`
+    lowest RoPE frequencies, so it is position-independent); V = vmean mu +
+    z W_v + v_noise eps.  ``heads`` restricts generation to a list of global
+    q-heads (their kv-heads too); every head is seeded by its global index,
+    so a subset equals the same slice of the full tensor."""
+    group = Hq // Hkv
+    hq_list = list(range(Hq)) if heads is None else list(heads)
+    kv_list = sorted({h // group for h in hq_list})
+    q = np.empty((B, len(hq_list), N, d), np.float32)
+    k = np.empty((B, len(kv_list), N, d), np.float32)
+    v = np.empty((B, len(kv_list), N, d), np.float32)
+    h2 = d // 2
+    low = np.r_[h2 - sink_pairs:h2, d - sink_pairs:d]       # lowest-frequency pairs
+    for b in range(B):
+        for a, g_kv in enumerate(kv_list):
+            g = _rng([seed, b, 2000 + g_kv])
+            c = g.standard_normal(d)
+            z = _ar1(g, N, d, rho)
+            wk = g.standard_normal((d, d)) / math.sqrt(d)
+            kc = c + head_jitter * g.standard_normal(d) + alpha * (z @ wk) \
+                + noise * g.standard_normal((N, d))
+            kk = gamma * rope(kc, base)
+            # sink: q_t . k_0 / sqrt(d) ~ sink * gamma^2 |c|^2 / sqrt(d) for every t
+            s0 = np.zeros(d)
+            s0[low] = c[low] * (d / (2 * sink_pairs)) * sink
+            kk[0] = gamma * s0
+            k[b, a] = kk
+            mu = g.standard_normal(d)
+            wv = g.standard_normal((d, d)) / math.sqrt(d)
+            v[b, a] = vmean * mu[None, :] + z @ wv + v_noise * g.standard_normal((N, d))
+            for h in range(g_kv * group, (g_kv + 1) * group):
+                if h not in hq_list:
+                    continue
+                gh = _rng([seed, b, 3000 + h])
+                wq = wk + head_jitter * gh.standard_normal((d, d)) / math.sqrt(d)
+                qc = c + head_jitter * gh.standard_normal(d) + alpha * (z @ wq) \
+                    + noise * gh.standard_normal((N, d))
+                q[b, hq_list.index(h)] = gamma * rope(qc, base)
+    return q, k, v
+
+
 def video(seed, T, H, W, d=64, heads=30, text_prefix=0, B=1, gamma=1.0, noise=0.35,
           n_waves=8, corr_len=6.0, head_jitter=0.4, heads_subset=None):
     """C3 / C4: tokens [text_prefix i.i.d. text][T*H*W video, (t,h,w) row-major]."""
@@ -154,7 +226,7 @@ def to_device(x, dtype=None, device="cuda", pin=False):
 # BASELINE.json configs[0]'s values for every config (reading R20).
 WORKLOADS = {
     "planted_c1": dict(kind="planted", N=1024, d=64, Hq=1, Hkv=1, causal=False),
-    "llama31_8b_32k": dict(kind="llm_local", N=32768, d=128, Hq=32, Hkv=8, causal=True),
+    "llama31_8b_32k": dict(kind="llm_rope", N=32768, d=128, Hq=32, Hkv=8, causal=True),
     "cogvideox_2b": dict(kind="video", T=13, H=30, W=45, text_prefix=226, d=64, Hq=30,
                          Hkv=30, causal=False, hilbert=True),
     "mochi": dict(kind="video", T=28, H=30, W=53, text_prefix=0, d=128, Hq=24, Hkv=24,
@@ -162,10 +234,15 @@ WORKLOADS = {
     # the paper's own Mochi run is ~22K tokens: half the latent frames
     "mochi_22k": dict(kind="video", T=14, H=30, W=53, text_prefix=0, d=128, Hq=24, Hkv=24,
                       causal=False, hilbert=True),
-    "sweep_8k": dict(kind="llm_local", N=8192, d=128, Hq=32, Hkv=32, causal=False),
-    "sweep_16k": dict(kind="llm_local", N=16384, d=128, Hq=32, Hkv=32, causal=False),
-    "sweep_32k": dict(kind="llm_local", N=32768, d=128, Hq=32, Hkv=32, causal=False),
-    "sweep_64k": dict(kind="llm_local", N=65536, d=128, Hq=32, Hkv=32, causal=False),
-    "sweep_128k": dict(kind="llm_local", N=131072, d=128, Hq=32, Hkv=32, causal=False),
+    # Flux (Table 1 "Flux (4.5K)"): 512 text tokens + a 64 x 64
+    # latent patch grid (1024 x 1024 image, 16x VAE x 2x2 patches), 24 heads,
+    # d = 128, joint non-causal attention; the image tokens Hilbert-ordered
+    "flux": dict(kind="video", T=1, H=64, W=64, text_prefix=512, d=128, Hq=24, Hkv=24,
+                 causal=False, hilbert=True),
+    "sweep_8k": dict(kind="llm_rope", N=8192, d=128, Hq=32, Hkv=32, causal=False),
+    "sweep_16k": dict(kind="llm_rope", N=16384, d=128, Hq=32, Hkv=32, causal=False),
+    "sweep_32k": dict(kind="llm_rope", N=32768, d=128, Hq=32, Hkv=32, causal=False),
+    "sweep_64k": dict(kind="llm_rope", N=65536, d=128, Hq=32, Hkv=32, causal=False),
+    "sweep_128k": dict(kind="llm_rope", N=131072, d=128, Hq=32, Hkv=32, causal=False),
 }
 HYPER = dict(tau=0.9, theta=0.5, lam=-5.0)
