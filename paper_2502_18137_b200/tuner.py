@@ -25,7 +25,7 @@ input, a2 + a3 per candidate, L1 by `sparge_l1_sums`).
 
 import math
 
-DEFAULT_TAU_GRID = (0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.98, 1.0)
+DEFAULT_TAU_GRID = (0.5, 0.6, 0.7, 0.75, 0.8, 0.84, 0.88, 0.9, 0.92, 0.94, 0.96, 0.98, 1.0)
 DEFAULT_THETA_GRID = (-1.0, 0.0, 0.2, 0.4, 0.6, 0.8)          # -1 = judge off
 DEFAULT_LAMBDA_GRID = (-math.inf, -20.0, -15.0, -10.0, -8.0, -6.0, -5.0, -4.0)
 
