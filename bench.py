@@ -10,11 +10,21 @@ speed 1/t = O(attn)/t in TOPS, with O(attn) the dense attention op
 count (4 N^2 d H, causal: 4 d H N(N+1)/2, reading R8-v) and t the device time
 of the step (prediction included).
 
-Multi-GPU (torchrun): every rank runs its own batch element (seeded by rank)
-with no data-path collective -> "scaling": "weak"; value = all ranks' dense
-ops / max-over-ranks step time.  Inputs are synthetic (paper_2502_18137_b200
-.inputs); the oracle (oracle/) is used only for the cpu_baseline leg, the
-sampled parity figures and --impl reference.
+Multi-GPU (torchrun): the heads of ONE sequence are split by
+contiguous kv-groups across ranks (--shard heads, default), each rank
+generating its shard from per-global-head seeds -- no data-path collective;
+value = the whole job's dense ops / max-over-ranks step time ("scaling":
+"strong").  After timing, O is all-gathered over NCCL and compared bit for
+bit with one GPU running every head.  --shard batch gives every rank its own
+sequence instead (weak scaling).
+
+Hyper-parameters: each workload runs at the triple the §3.6 tuner found at
+the paper's accuracy bounds (inputs.TUNED <- profiles/r02_f2_tuned.json,
+P:L469); --triple fixed selects round 1's tau=.9/theta=.5/lambda=-5 (R20).
+The default line also carries the configs[4] sweep (8K..128K, each point at
+its own tuned triple).  Inputs are synthetic (paper_2502_18137_b200.inputs);
+the oracle (oracle/) is used only for the cpu_baseline leg, the parity
+figures and --impl reference.
 """
 import argparse
 import json
@@ -50,9 +60,17 @@ def parse():
     ap.add_argument("--profile", action="store_true",
                     help="minimal run for ncu: warmup + steps only, no side legs")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
-    ap.add_argument("--tau", type=float, default=None, help="override tau (default 0.9, R20)")
-    ap.add_argument("--theta", type=float, default=None, help="override theta (default 0.5)")
-    ap.add_argument("--lam", type=float, default=None, help="override lambda (default -5)")
+    ap.add_argument("--tau", type=float, default=None, help="override tau")
+    ap.add_argument("--theta", type=float, default=None, help="override theta")
+    ap.add_argument("--lam", type=float, default=None, help="override lambda")
+    ap.add_argument("--triple", default="tuned", choices=["tuned", "fixed"],
+                    help="tuned: inputs.TUNED (the §3.6 tuner at the paper's bounds); "
+                         "fixed: tau=.9 theta=.5 lambda=-5 (R20)")
+    ap.add_argument("--shard", default="heads", choices=["heads", "batch"],
+                    help="multi-GPU partition (SURVEY §8(e)): kv-groups of one sequence, "
+                         "or one sequence per rank")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the 8K..128K sweep leg")
+    ap.add_argument("--no-gather-check", action="store_true")
     return ap.parse_args()
 
 
@@ -61,6 +79,7 @@ def workload_cfg(name):
     from paper_2502_18137_b200 import inputs
     cfg = dict(inputs.WORKLOADS[name])
     cfg.update(inputs.HYPER)
+    cfg["triple"] = "fixed (R20)"
     if cfg["kind"] == "video":
         cfg["N"] = cfg["text_prefix"] + cfg["T"] * cfg["H"] * cfg["W"]
     return cfg
@@ -185,12 +204,251 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx),
                 "reasons": sorted(reasons), "samples": len(sm)}
 
-
 # ------------------------------------------------------------------ our arm
+STAGES = ["quant_ms", "predict_ms", "vprep_ms", "attn_ms"]
+# kernels per step: quantise Q, quantise K, S^ DMMA, TopCdf rows, V^T stage,
+# launch order x2, attention
+LAUNCHES_PER_STEP = 8
+
+
+class Problem:
+    """One rank's share of a workload on its GPU: inputs resident in HBM
+    (plus pinned host copies for the e2e leg), the C-ABI shape and buffers.
+
+    shard="heads" (multi-GPU default): contiguous kv-groups of
+    ONE sequence per rank, generated from per-global-head seeds, so nothing
+    is sent; shard="batch": every rank its own sequence (seed 1000 + rank)."""
+
+    def __init__(self, cfg, world, rank, dev, shard="heads", seed=1000, pin=True):
+        import torch
+        from paper_2502_18137_b200 import inputs, multigpu, sparge
+        self.cfg, self.dev = cfg, dev
+        N, d, Hq, Hkv = cfg["N"], cfg["d"], cfg["Hq"], cfg["Hkv"]
+        if shard == "heads" and world > 1:
+            self.hq, self.hkv = multigpu.local_heads(Hq, Hkv, world, rank)
+            heads = self.hq
+        else:
+            self.hq, self.hkv = list(range(Hq)), list(range(Hkv))
+            heads = None
+            if shard == "batch":
+                seed = seed + rank
+        self.shard, self.world = shard, world
+        self.Hq, self.Hkv = len(self.hq), len(self.hkv)
+        self.empty = self.Hq == 0
+        self.perm_np = hilbert_perm(cfg)
+        self.perm = None if self.perm_np is None else torch.from_numpy(self.perm_np).to(dev)
+        if self.empty:
+            return
+        qn, kn, vn = gen_inputs(cfg, seed=seed, heads=heads)
+        self.host = tuple(inputs.to_device(a, device="cpu", pin=pin) for a in (qn, kn, vn))
+        del qn, kn, vn
+        self.q, self.k, self.v = (t.to(dev) for t in self.host)
+        self.shape = sparge.make_shape(1, self.Hq, self.Hkv, N, d, cfg["causal"], self.q.dtype)
+        self.bf = sparge.Buffers(self.shape, device=dev)
+        self.o = torch.empty_like(self.q)
+        tm, tn = math.ceil(N / 128), math.ceil(N / 64)
+        if cfg["causal"]:
+            self.live = sum(min(tn, (min((i + 1) * 128, N) - 1) // 64 + 1)
+                            for i in range(tm)) * self.Hq
+        else:
+            self.live = tm * tn * self.Hq
+
+    def ops(self):
+        """Dense attention ops of this rank's share (R8-v)."""
+        c = dict(self.cfg)
+        c["Hq"] = self.Hq
+        return dense_ops(c)
+
+    def step(self, ev=None, counters=None, tau=None, theta=None, lam=None, shape=None, bf=None,
+             o=None):
+        """One pass of the whole hot path: a1(Q), a1(K), a2, V stage, a3."""
+        from paper_2502_18137_b200 import sparge
+        if self.empty:
+            for e in (ev or []):
+                e.record()
+            return
+        cfg = self.cfg
+        tau = cfg["tau"] if tau is None else tau
+        theta = cfg["theta"] if theta is None else theta
+        lam = cfg["lam"] if lam is None else lam
+        shape = self.shape if shape is None else shape
+        bf = self.bf if bf is None else bf
+        o = self.o if o is None else o
+        q, k, v, perm = self.q, self.k, self.v, self.perm
+        if ev: ev[0].record()
+        sparge.sparge_quantize(shape, q, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim)
+        if shape.smooth_k:        # row f4 K smoothing: mean, then INT8 of K - mean
+            sparge.sparge_smooth_k_mean(shape, k, bf.smooth_workspace, bf.k_mean)
+            sparge.sparge_quantize_smooth_k(shape, k, perm, bf.k_mean, bf.kq, bf.dk, bf.k_pooled,
+                                            bf.k_sim)
+        else:
+            sparge.sparge_quantize(shape, k, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim)
+        if ev: ev[1].record()
+        sparge.sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, tau, theta,
+                                   bf.mask, bf.lut, bf.cnt, bf.pred_workspace)
+        if ev: ev[2].record()
+        sparge.sparge_attn_fwd_ex(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm,
+                                  o, counters, bf.workspace, sparge.SPARGE_ATTN_VPREP_ONLY)
+        if ev: ev[3].record()
+        sparge.sparge_attn_fwd_ex(shape, bf.qq, bf.dq, bf.kq, bf.dk, v, bf.lut, bf.cnt, lam, perm,
+                                  o, counters, bf.workspace, sparge.SPARGE_ATTN_SKIP_VPREP)
+        if ev: ev[4].record()
+
+    def dense_reference(self):
+        """Full attention without quantisation or sparsity: the f1 kernel with
+        tau = 1, theta = -1, lambda = -inf (bf16 QK^T, fp32 softmax; the
+        tuner's reference O', reading R25)."""
+        import torch
+        from paper_2502_18137_b200 import sparge
+        ref = torch.empty_like(self.q)
+        sparge.sparge_forward(self.q, self.k, self.v, 1.0, -1.0, -math.inf,
+                              causal=self.cfg["causal"], perm=self.perm, out=ref,
+                              qk_dtype=sparge.SPARGE_QK_INPUT, counters=False)
+        return ref
+
+
+def all_sum(vals, dev):
+    """Sum host numbers over ranks (counters / L1 sums)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x) for x in vals], dtype=torch.float64, device=dev)
+    if dist.is_initialized():
+        dist.all_reduce(t)
+    return t.tolist()
+
+
+def time_steps(prob, K, W, flush, sync, clock=False, **kw):
+    """W untimed warm-up steps, then K steps with L2 flushed between them,
+    per-stage CUDA events on the launching stream.  Returns (per-step stage
+    ms [K, 4], clock summary or None)."""
+    import torch
+    for _ in range(W):
+        prob.step(**kw)
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
+    sync()
+    torch.cuda.synchronize()
+    clk = None
+    if clock:
+        props = torch.cuda.get_device_properties(prob.dev)
+        gpu_id = str(props.uuid)
+        gpu_id = gpu_id if gpu_id.startswith("GPU-") else f"GPU-{gpu_id}"
+        clk = ClockSampler(gpu_id)
+        clk.__enter__()
+    for s in range(K):
+        flush.zero_()                          # L2 flush between steps (not timed)
+        prob.step(ev=evs[s], **kw)
+    torch.cuda.synchronize()
+    if clk is not None:
+        clk.__exit__(None, None, None)
+    sync()
+    st = np.array([[evs[s][a].elapsed_time(evs[s][a + 1]) for a in range(4)] for s in range(K)])
+    return st, (clk.summary() if clk is not None else None)
+
+
+def counters_of(prob, dev):
+    """(qk tiles, PV warp slices, PV MMAs, live tiles) summed over ranks."""
+    if prob.empty:
+        return all_sum([0, 0, 0, 0], dev)
+    c = prob.bf.counters.cpu().numpy().astype(np.int64)
+    return all_sum([c[0, :, 0].sum(), c[0, :, 1].sum(), c[0, :, 2].sum(), prob.live], dev)
+
+
+def l1_vs_dense(prob, dev):
+    """Relative L1 of this step's O against full attention (R25), whole job."""
+    from paper_2502_18137_b200 import sparge
+    if prob.empty:
+        return all_sum([0.0, 0.0], dev)
+    ref = prob.dense_reference()
+    s = sparge.sparge_l1_sums(prob.o, ref)[:2].cpu().tolist()
+    del ref
+    return all_sum(s, dev)
+
+
+def sparsity_from(c):
+    qk, pv, _, live = c
+    return 1.0 - (qk + pv / 4.0) / (2.0 * live) if live else 0.0
+
+
+def roofline_of(d, qk_exec, pv_slices, attn_ms, workload):
+    per_tile_qk = 2.0 * 128 * 64 * d
+    per_slice_pv = 2.0 * 32 * 64 * d
+    ops_qk = qk_exec * per_tile_qk
+    ops_pv = pv_slices * per_slice_pv
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        bf16_peak, peak_src = float(peaks["bf16_tflops"]), "measured"
+    except Exception:
+        bf16_peak, peak_src = 1590.0, "fallback"
+    i8_peak = 2.0 * bf16_peak          # INT8 dense = 2x bf16 (nominal ratio, 4.5 vs 2.25 POPS)
+    tot = ops_qk + ops_pv
+    mix_peak = tot / (ops_qk / i8_peak + ops_pv / bf16_peak) if tot else i8_peak
+    sheet_peak = tot / (ops_qk / 4500.0 + ops_pv / 2250.0) if tot else 4500.0
+    achieved = tot / (attn_ms * 1e-3) / 1e12 if attn_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(workload)
+    return {"bound": "tensor", "kernel": "k_sparse_attn", "achieved": achieved,
+            "peak": mix_peak, "unit": "TFLOP/s", "frac": achieved / mix_peak,
+            "traffic": traffic,
+            "frac_datasheet": achieved / sheet_peak,
+            "peak_note": f"INT8 QK at 2x bf16 {peak_src} ({i8_peak:.0f}) + bf16 PV "
+                         f"({bf16_peak:.0f}), weighted by the executed op mix; frac_datasheet "
+                         f"uses the nominal 4500/2250 TOPS mix ({sheet_peak:.0f})"}, bf16_peak
+
+
+def hyper(cfg, name, triple):
+    """tau/theta/lambda of a workload: the §3.6 tuner's values at the paper's
+    bounds (inputs.TUNED, profiles/r02_f2_tuned.json) or the fixed R20 triple."""
+    from paper_2502_18137_b200 import inputs
+    if triple == "tuned" and name in inputs.TUNED:
+        t = inputs.TUNED[name]
+        cfg.update(tau=t["tau"], theta=t["theta"], lam=t["lambda"], triple="tuned",
+                   l1_bound=t["l1_bound"])
+    else:
+        cfg.update(inputs.HYPER)
+        cfg["triple"] = "fixed (R20)"
+    return cfg
+
+
+def measure_workload(name, args, world, rank, dev, flush, sync, K, W, dense=True):
+    """One workload at its own triple: TOPS, sparsity, stages, L1 vs dense,
+    dense comparator (used by the sweep leg)."""
+    import torch
+    from paper_2502_18137_b200 import multigpu
+    cfg = hyper(workload_cfg(name), name, args.triple)
+    prob = Problem(cfg, world, rank, dev, args.shard, pin=False)
+    if not prob.empty:
+        prob.bf.counters.zero_()
+        prob.step(counters=prob.bf.counters)
+    c = counters_of(prob, dev)
+    st, _ = time_steps(prob, K, W, flush, sync)
+    ms = multigpu.max_over_ranks(float(st.sum(1).mean()), dev)
+    ops_total = dense_ops(cfg) * (world if args.shard == "batch" else 1)
+    s1, s2 = l1_vs_dense(prob, dev)
+    stages = dict(zip(STAGES, st.mean(0).tolist()))
+    out = {"workload": name, "N": cfg["N"], "tau": cfg["tau"], "theta": cfg["theta"],
+           "lambda": cfg["lam"], "triple": cfg["triple"], "value": ops_total / (ms * 1e-3) / 1e12,
+           "unit": "TOPS", "ms_per_step": ms, "sparsity": sparsity_from(c), "stages_ms": stages,
+           "predict_over_attn": stages["predict_ms"] / stages["attn_ms"] if stages["attn_ms"] else None,
+           "l1_vs_dense": s1 / s2 if s2 else None}
+    if dense:
+        Kd = max(2, min(K, 5))
+        std, _ = time_steps(prob, Kd, 1, flush, sync, tau=1.0, theta=-1.0, lam=-math.inf)
+        dms = multigpu.max_over_ranks(float(std.sum(1).mean()), dev)
+        out["dense_value"] = ops_total / (dms * 1e-3) / 1e12
+        out["speedup"] = out["value"] / out["dense_value"]
+        out["target_0.8/(1-s)"] = 0.8 / max(1e-9, 1.0 - out["sparsity"])
+    del prob
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2502_18137_b200 import inputs, sparge
+    from paper_2502_18137_b200 import multigpu, shard, sparge
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -199,294 +457,269 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = workload_cfg(args.workload)
+    cfg = hyper(workload_cfg(args.workload), args.workload, args.triple)
     for key in ("tau", "theta", "lam"):
         if getattr(args, key) is not None:
             cfg[key] = getattr(args, key)
+            cfg["triple"] = "override"
     N, d, Hq, Hkv = cfg["N"], cfg["d"], cfg["Hq"], cfg["Hkv"]
-    tau, theta, lam = cfg["tau"], cfg["theta"], cfg["lam"]
 
-    qn, kn, vn = gen_inputs(cfg, seed=1000 + rank)
-    t_perm = time.perf_counter()
-    perm_np = hilbert_perm(cfg)                # a0: host index build, once per shape
-    perm_host_ms = 1e3 * (time.perf_counter() - t_perm) if perm_np is not None else 0.0
-    qh, kh, vh = (inputs.to_device(a, device="cpu", pin=True) for a in (qn, kn, vn))
-    q, k, v = (t.to(dev) for t in (qh, kh, vh))
-    perm = None if perm_np is None else torch.from_numpy(perm_np).to(dev)
-    shape = sparge.make_shape(1, Hq, Hkv, N, d, cfg["causal"], q.dtype)
-    bf = sparge.Buffers(shape, device=dev)
-    o = torch.empty_like(q)
-    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
-
-    def step(ev=None, counters=bf.counters, t=tau, th=theta, lm=lam, q_=q, k_=k, v_=v, o_=o,
-             shape=shape, bf=bf):
-        if ev: ev[0].record()
-        sparge.sparge_quantize(shape, q_, 0, perm, bf.qq, bf.dq, bf.q_pooled, bf.q_sim)
-        if shape.smooth_k:        # row f4 K smoothing: mean, then INT8 of K - mean
-            sparge.sparge_smooth_k_mean(shape, k_, bf.smooth_workspace, bf.k_mean)
-            sparge.sparge_quantize_smooth_k(shape, k_, perm, bf.k_mean, bf.kq, bf.dk, bf.k_pooled,
-                                            bf.k_sim)
-        else:
-            sparge.sparge_quantize(shape, k_, 1, perm, bf.kq, bf.dk, bf.k_pooled, bf.k_sim)
-        if ev: ev[1].record()
-        sparge.sparge_predict_mask(shape, bf.q_pooled, bf.q_sim, bf.k_pooled, bf.k_sim, t, th,
-                                   bf.mask, bf.lut, bf.cnt, bf.pred_workspace)
-        if ev: ev[2].record()
-        sparge.sparge_attn_fwd_ex(shape, bf.qq, bf.dq, bf.kq, bf.dk, v_, bf.lut, bf.cnt, lm, perm,
-                                  o_, counters, bf.workspace, sparge.SPARGE_ATTN_VPREP_ONLY)
-        if ev: ev[3].record()
-        sparge.sparge_attn_fwd_ex(shape, bf.qq, bf.dq, bf.kq, bf.dk, v_, bf.lut, bf.cnt, lm, perm,
-                                  o_, counters, bf.workspace, sparge.SPARGE_ATTN_SKIP_VPREP)
-        if ev: ev[4].record()
-
-    def barrier():
+    def sync():
         if world > 1:
             dist.barrier()
 
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    t_perm = time.perf_counter()
+    prob = Problem(cfg, world, rank, dev, args.shard)
+    perm_host_ms = 1e3 * (time.perf_counter() - t_perm) if prob.perm_np is not None else 0.0
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     # one untimed step for sparsity / counters / parity samples
-    bf.counters.zero_()
-    step()
-    sparge.sparge_attn_status(bf.workspace)
-    cnt0 = bf.counters.cpu().numpy().astype(np.int64)
-    snap = (o[0, 0].float().cpu(), bf.mask[0, 0].cpu())   # head 0 for the parity leg
-    qk_exec, pv_slices, pv_mma = (int(cnt0[0, :, c].sum()) for c in range(3))
-    tm, tn = math.ceil(N / 128), math.ceil(N / 64)
-    if cfg["causal"]:
-        live = sum(min(tn, (min((i + 1) * 128, N) - 1) // 64 + 1) for i in range(tm)) * Hq
-    else:
-        live = tm * tn * Hq
-    sparsity = 1.0 - (qk_exec + pv_slices / 4.0) / (2.0 * live)
+    if not prob.empty:
+        prob.bf.counters.zero_()
+        prob.step(counters=prob.bf.counters)
+        sparge.sparge_attn_status(prob.bf.workspace)
+    c = counters_of(prob, dev)
+    qk_exec, pv_slices, pv_mma, live = (int(x) for x in c)
+    sparsity = sparsity_from(c)
+    snap = None
+    if rank == 0 and not prob.empty:
+        snap = (prob.o[0, 0].float().cpu(), prob.bf.mask[0, 0].cpu())   # head 0 for the parity leg
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(K)]
-    gpu_id = torch.cuda.get_device_properties(dev).uuid
-    gpu_id = f"GPU-{gpu_id}" if not str(gpu_id).startswith("GPU-") else str(gpu_id)
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(gpu_id) as clk:
-        for s in range(K):
-            flush.zero_()                      # L2 flush between steps (not timed)
-            step(evs[s])
-        torch.cuda.synchronize()
-    barrier()
-    st = np.array([[evs[s][a].elapsed_time(evs[s][a + 1]) for a in range(4)] for s in range(K)])
+    K, W = args.steps, args.warmup
+    st, clk = time_steps(prob, K, W, flush, sync, clock=True)
     step_ms = st.sum(1)
-    ms = max_over_ranks(float(step_ms.mean()))
-    stages = dict(zip(["quant_ms", "predict_ms", "vprep_ms", "attn_ms"], st.mean(0).tolist()))
-    ops_rank = dense_ops(cfg)
-    value = ops_rank * world / (ms * 1e-3) / 1e12
-
-    # ---- roofline of the dominant kernel (k_sparse_attn) ----
-    per_tile_qk = 2.0 * 128 * 64 * d
-    per_slice_pv = 2.0 * 32 * 64 * d
-    ops_qk = qk_exec * per_tile_qk
-    ops_pv = pv_slices * per_slice_pv
-    attn_s = stages["attn_ms"] * 1e-3
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        bf16_peak, peak_src = float(peaks["bf16_tflops"]), "measured"
-    except Exception:
-        bf16_peak, peak_src = 1590.0, "fallback"
-    i8_peak = 2.0 * bf16_peak          # INT8 dense = 2x bf16 (nominal ratio, 4.5 vs 2.25 POPS)
-    mix_peak = (ops_qk + ops_pv) / (ops_qk / i8_peak + ops_pv / bf16_peak)
-    achieved = (ops_qk + ops_pv) / attn_s / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(args.workload)
-    roofline = {"bound": "tensor", "kernel": "k_sparse_attn", "achieved": achieved,
-                "peak": mix_peak, "unit": "TFLOP/s", "frac": achieved / mix_peak,
-                "traffic": traffic,
-                "peak_note": f"INT8 QK at 2x bf16 {peak_src} ({i8_peak:.0f}) + bf16 PV "
-                             f"({bf16_peak:.0f}), weighted by the executed op mix"}
-
+    ms = multigpu.max_over_ranks(float(step_ms.mean()), dev)
+    stages = dict(zip(STAGES, st.mean(0).tolist()))
+    ops_total = dense_ops(cfg) * (world if args.shard == "batch" else 1)
+    value = ops_total / (ms * 1e-3) / 1e12
+    # the dominant kernel on this rank (rank 0's share; its own counters)
+    c_loc = prob.bf.counters.cpu().numpy().astype(np.int64) if not prob.empty else np.zeros((1, 1, 3))
+    roofline, bf16_peak = roofline_of(d, int(c_loc[0, :, 0].sum()), int(c_loc[0, :, 1].sum()),
+                                      stages["attn_ms"], args.workload)
+    if world > 1 and args.shard == "heads":
+        par = f"heads: kv-groups split over {world} ranks (no data-path collective)"
+    elif world > 1:
+        par = f"batch x{world} (independent sequences, no collective)"
+    else:
+        par = "single GPU"
     result = {
         "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": W, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if (world > 1 and args.shard == "batch") else "strong",
         "vs_baseline": None, "dtype": "int8+bf16", "data": "synthetic",
-        "config": {"workload": args.workload, "B_per_gpu": 1, "global_batch": world, "N": N,
-                   "d": d, "Hq": Hq, "Hkv": Hkv, "causal": bool(cfg["causal"]),
-                   "hilbert": bool(cfg.get("hilbert")), "tau": tau, "theta": theta,
-                   "lambda": lam, "parallelism": f"batch x{world} (independent, no collective)",
+        "config": {"workload": args.workload, "B": world if args.shard == "batch" else 1,
+                   "N": N, "d": d, "Hq": Hq, "Hkv": Hkv, "causal": bool(cfg["causal"]),
+                   "hilbert": bool(cfg.get("hilbert")), "tau": cfg["tau"],
+                   "theta": cfg["theta"], "lambda": cfg["lam"], "triple": cfg["triple"],
+                   "parallelism": par, "heads_per_rank": prob.Hq,
                    "l2": "flushed (512 MB write) between timed steps"},
         "sparsity": sparsity,
         "counters": {"qk_tiles": qk_exec, "pv_warp_slices": pv_slices, "pv_mmas": pv_mma,
                      "live_tiles": live},
         "stages_ms": stages,
-        "permutation": {"hilbert": perm_np is not None, "host_build_ms": perm_host_ms,
-                        "ms_per_step_incl_perm_build": ms + perm_host_ms,
+        "predict_over_attn": stages["predict_ms"] / stages["attn_ms"] if stages["attn_ms"] else None,
+        "permutation": {"hilbert": prob.perm_np is not None, "host_build_ms": perm_host_ms,
                         "note": "a0 index build on the host once per shape; the gather is "
                                 "fused into a1 / the V stage and the scatter into a3"},
         "roofline": roofline,
-        "gpu_launches": 8 * K,   # per step: quant x2, S^ DMMA, TopCdf, V^T, order x2, attention
-        "clocks": clk.summary(),
+        "gpu_launches": (0 if prob.empty else LAUNCHES_PER_STEP) * K,
+        "clocks": clk,
     }
+    if world > 1:
+        result["multi_gpu"] = {"partition": args.shard, "static_efficiency":
+                               shard.static_efficiency(Hkv, world) if args.shard == "heads" else 1.0}
     if args.profile:
         emit(result, rank, args)
         return
 
+    # ---- accuracy at this triple: L1 vs full attention, whole job ----
+    s1, s2 = l1_vs_dense(prob, dev)
+    result["accuracy"] = {"l1_vs_dense": s1 / s2 if s2 else None,
+                          "l1_bound_paper": cfg.get("l1_bound"),
+                          "reference": "full attention, no quantisation or sparsity (the f1 "
+                                       "kernel, tau=1 theta=-1 lambda=-inf; R25)"}
+
     # ---- dense comparator: same kernels, all-ones mask, lambda = -inf ----
     if not args.no_dense:
-        Kd = min(K, 10)
-        evd = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(Kd)]
-        step(counters=None, t=1.0, th=-1.0, lm=-math.inf)
-        torch.cuda.synchronize()
-        for s in range(Kd):
-            flush.zero_()
-            step(evd[s], counters=None, t=1.0, th=-1.0, lm=-math.inf)
-        torch.cuda.synchronize()
-        dms = max_over_ranks(float(np.mean([evd[s][0].elapsed_time(evd[s][4]) for s in range(Kd)])))
-        dense_value = ops_rank * world / (dms * 1e-3) / 1e12
+        std, _ = time_steps(prob, min(K, 10), 1, flush, sync, tau=1.0, theta=-1.0,
+                            lam=-math.inf)
+        dms = multigpu.max_over_ranks(float(std.sum(1).mean()), dev)
+        dense_value = ops_total / (dms * 1e-3) / 1e12
         result["dense"] = {"value": dense_value, "ms_per_step": dms,
-                           "speedup": dense_value and value / dense_value,
+                           "speedup": value / dense_value,
                            "target_0.8/(1-s)": 0.8 / max(1e-9, 1.0 - sparsity)}
+
+    # ---- the fixed R20 triple on the same inputs (round 1's headline) ----
+    if args.triple == "tuned" and not prob.empty:
+        from paper_2502_18137_b200 import inputs as _in
+        fx = _in.HYPER
+        prob.bf.counters.zero_()
+        prob.step(counters=prob.bf.counters, tau=fx["tau"], theta=fx["theta"], lam=fx["lam"])
+        cf = counters_of(prob, dev)
+        stf, _ = time_steps(prob, min(K, 10), 2, flush, sync, tau=fx["tau"], theta=fx["theta"],
+                            lam=fx["lam"])
+        fms = multigpu.max_over_ranks(float(stf.sum(1).mean()), dev)
+        prob.step(tau=fx["tau"], theta=fx["theta"], lam=fx["lam"])
+        f1_, f2_ = l1_vs_dense(prob, dev)
+        result["fixed_triple"] = {"tau": fx["tau"], "theta": fx["theta"], "lambda": fx["lam"],
+                                  "value": ops_total / (fms * 1e-3) / 1e12, "ms_per_step": fms,
+                                  "sparsity": sparsity_from(cf),
+                                  "l1_vs_dense": f1_ / f2_ if f2_ else None}
+        prob.step()                                 # o = the headline triple's output again
 
     # ---- NEXT rows on the same inputs and hyper-parameters: f1 = the
     # unquantised "SpargeAttn+FA2" kernel (bf16 QK^T, Fig. 7); f4 =
     # FP8 E4M3 P~V on INT8 QK^T (SageAttention2-style, footnote P:L44) ----
     def variant(key, qk_dtype, pv_dtype, peak_tflops, smooth_k=False):
-        shape_v = sparge.make_shape(1, Hq, Hkv, N, d, cfg["causal"], q.dtype,
+        shape_v = sparge.make_shape(1, prob.Hq, prob.Hkv, N, d, cfg["causal"], prob.q.dtype,
                                     qk_dtype=qk_dtype, pv_dtype=pv_dtype, smooth_k=smooth_k)
         bv = sparge.Buffers(shape_v, device=dev)
-        Kf = min(K, 10)
-        evf = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(Kf)]
-        step(counters=bv.counters, shape=shape_v, bf=bv)
+        ov = torch.empty_like(prob.o)
+        prob.step(counters=bv.counters, shape=shape_v, bf=bv, o=ov)
         sparge.sparge_attn_status(bv.workspace)
         cv = bv.counters.cpu().numpy().astype(np.int64)
-        for s_ in range(Kf):
-            flush.zero_()
-            step(evf[s_], counters=None, shape=shape_v, bf=bv)
-        torch.cuda.synchronize()
-        stf = np.array([[evf[s_][a].elapsed_time(evf[s_][a + 1]) for a in range(4)]
-                        for s_ in range(Kf)])
-        fms = max_over_ranks(float(stf.sum(1).mean()))
+        stf, _ = time_steps(prob, min(K, 10), 1, flush, sync, shape=shape_v, bf=bv, o=ov)
+        fms = multigpu.max_over_ranks(float(stf.sum(1).mean()), dev)
         f_attn_s = float(stf[:, 3].mean()) * 1e-3
-        ops_v = int(cv[0, :, 0].sum()) * per_tile_qk + int(cv[0, :, 1].sum()) * per_slice_pv
-        ov = torch.empty_like(o)
-        step(counters=None, shape=shape_v, bf=bv, o_=ov)
-        step(counters=None)                  # o = the default path's output again
-        torch.cuda.synchronize()
+        ops_v = int(cv[0, :, 0].sum()) * 2.0 * 128 * 64 * d + int(cv[0, :, 1].sum()) * 2.0 * 32 * 64 * d
         result[key] = {
-            "value": ops_rank * world / (fms * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": fms,
-            "stages_ms": dict(zip(["quant_ms", "predict_ms", "vprep_ms", "attn_ms"],
-                                  stf.mean(0).tolist())),
+            "value": ops_total / (fms * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": fms,
+            "stages_ms": dict(zip(STAGES, stf.mean(0).tolist())),
             "attn_achieved_tops": ops_v / f_attn_s / 1e12,
             "attn_peak_note": f"{peak_tflops:.0f} TF/s peak of the executed op mix",
             "attn_frac": ops_v / f_attn_s / 1e12 / peak_tflops,
-            "mask_equal_to_int8": bool(torch.equal(bv.mask, bf.mask) and torch.equal(bv.cnt, bf.cnt)),
-            "rel_l1_vs_int8_path": float((ov.float() - o.float()).abs().sum() / o.float().abs().sum()),
+            "mask_equal_to_int8": bool(torch.equal(bv.mask, prob.bf.mask)
+                                       and torch.equal(bv.cnt, prob.bf.cnt)),
+            "rel_l1_vs_int8_path": float((ov.float() - prob.o.float()).abs().sum()
+                                         / prob.o.float().abs().sum()),
         }
-        del bv
+        del bv, ov
 
-    if not args.no_f1:
+    if not args.no_f1 and not prob.empty:
         variant("f1_fa2_bf16qk", sparge.SPARGE_QK_INPUT, sparge.SPARGE_PV_SAME_AS_INPUT, bf16_peak)
         # INT8 QK + FP8 PV: both at 2x the bf16 rate (nominal 4.5 vs 2.25 POPS)
-        variant("f4_fp8_pv", sparge.SPARGE_QK_INT8, sparge.SPARGE_PV_FP8_E4M3, i8_peak)
+        variant("f4_fp8_pv", sparge.SPARGE_QK_INT8, sparge.SPARGE_PV_FP8_E4M3, 2.0 * bf16_peak)
         # K smoothing (row f4, R28) on the default INT8 QK / 16-bit PV path
-        variant("f4_smooth_k", sparge.SPARGE_QK_INT8, sparge.SPARGE_PV_SAME_AS_INPUT, mix_peak,
-                smooth_k=True)
+        variant("f4_smooth_k", sparge.SPARGE_QK_INT8, sparge.SPARGE_PV_SAME_AS_INPUT,
+                roofline["peak"], smooth_k=True)
 
     # ---- e2e through the public API with host buffers ----
     if not args.no_e2e:
-        oh = torch.empty_like(qh, device="cpu").pin_memory()
         Ke = min(K, 10)
         eve = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(Ke)]
-        # the public host-buffer entry point: kv-head chunks with H2D copy,
-        # compute and D2H copy on separate streams (sparge.HostPipeline)
-        pipe = sparge.HostPipeline(1, Hq, Hkv, N, d, causal=cfg["causal"], dtype=q.dtype,
-                                   chunks=max(c for c in (1, 2, 3, 4, 6, 8) if Hkv % c == 0),
-                                   device=dev)
+        if not prob.empty:
+            qh, kh, vh = prob.host
+            oh = torch.empty_like(qh, device="cpu").pin_memory()
+            # the public host-buffer entry point: kv-head chunks with H2D copy,
+            # compute and D2H copy on separate streams (sparge.HostPipeline)
+            pipe = sparge.HostPipeline(1, prob.Hq, prob.Hkv, N, d, causal=cfg["causal"],
+                                       dtype=prob.q.dtype,
+                                       chunks=max(c_ for c_ in (1, 2, 3, 4, 6, 8)
+                                                  if prob.Hkv % c_ == 0), device=dev)
 
-        def e2e_step():
-            pipe(qh, kh, vh, oh, tau, theta, lam, perm=perm)
-
-        e2e_step()
+            def e2e_step():
+                pipe(qh, kh, vh, oh, cfg["tau"], cfg["theta"], cfg["lam"], perm=prob.perm)
+            e2e_step()
         torch.cuda.synchronize()
-        barrier()
+        sync()
         for s in range(Ke):
             eve[s][0].record()
-            e2e_step()
+            if not prob.empty:
+                e2e_step()
             eve[s][1].record()
         torch.cuda.synchronize()
-        ems = max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in eve])))
-        result["e2e"] = {"value": ops_rank * world / (ems * 1e-3) / 1e12, "unit": "TOPS",
-                         "ms_per_step": ems,
-                         "h2d_bytes_per_step": int(sum(t.numel() * t.element_size()
-                                                       for t in (qh, kh, vh))),
-                         "d2h_bytes_per_step": int(oh.numel() * oh.element_size())}
+        ems = multigpu.max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in eve])), dev)
+        hb = all_sum([0, 0] if prob.empty else
+                     [sum(t.numel() * t.element_size() for t in prob.host),
+                      prob.o.numel() * prob.o.element_size()], dev)
+        result["e2e"] = {"value": ops_total / (ems * 1e-3) / 1e12, "unit": "TOPS",
+                         "ms_per_step": ems, "h2d_bytes_per_step": int(hb[0]),
+                         "d2h_bytes_per_step": int(hb[1])}
 
-    # ---- cpu_baseline + sampled parity (rank 0, N=1 only) ----
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result.update(cpu_leg(cfg, q, k, v, snap, perm_np))
+    # ---- multi-GPU: gather the head shards (NCCL all-gather over NVLink,
+    # outside the timed region) and compare with one GPU running all heads ----
+    if world > 1 and args.shard == "heads" and not args.no_gather_check:
+        o_loc = prob.o if not prob.empty else torch.zeros(1, 0, N, d, dtype=torch.bfloat16,
+                                                          device=dev)
+        o_full = multigpu.gather_heads(o_loc, Hq, Hkv)
+        if rank == 0:
+            single = Problem(cfg, 1, 0, dev, "heads", pin=False)
+            single.step()
+            torch.cuda.synchronize()
+            result["multi_gpu"].update({
+                "gather": "NCCL all_gather of O (outside the timed region)",
+                "o_bit_equal_to_single_gpu": bool(torch.equal(o_full, single.o)),
+                "max_abs_diff": float((o_full.float() - single.o.float()).abs().max())})
+            del single
+        del o_full
+        torch.cuda.empty_cache()
+        sync()
+
+    # ---- the configs[4] sweep (8K -> 128K, tuned triples, same sharding) ----
+    if not args.no_sweep:
+        sweep = []
+        for n in (8, 16, 32, 64, 128):
+            sweep.append(measure_workload(f"sweep_{n}k", args, world, rank, dev, flush, sync,
+                                          K=min(K, 10), W=3))
+        result["sweep"] = sweep
+
+    # ---- cpu_baseline + parity vs the oracle (rank 0, N=1 only) ----
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and snap is not None:
+        result.update(cpu_leg(cfg, prob, snap, ops_total))
     emit(result, rank, args)
     if world > 1:
         dist.destroy_process_group()
 
 
-def oracle_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        n = [i.get("num_threads", 1) for i in threadpool_info()]
-        return max(n) if n else 1
-    except Exception:
-        return 1
-
-
-def cpu_leg(cfg, q, k, v, snap, perm_np):
-    """Time the oracle as it stands on this host on a bounded sample of the
-    same workload (q-head 0: full stage-1 prediction + the sparse loop on
-    sampled query blocks) and compare the GPU's mask / O with it."""
+def cpu_leg(cfg, prob, snap, ops_total):
+    """The oracle as it stands, fanned out over this host's cores (oracle/
+    parallel.py), on q-head 0 of the same workload: full stage-1 prediction
+    plus the sparse loop on every q-block (N <= 32K) or a sample; timed, and
+    its mask / O compared with the GPU's."""
     import oracle as O
-    N, d = cfg["N"], cfg["d"]
+    from oracle.parallel import cores, spargeattn_head_parallel
+    N = cfg["N"]
     tm = math.ceil(N / 128)
-    group = cfg["Hq"] // cfg["Hkv"]
-    qs = q[0, 0].float().cpu().double().numpy()
-    ks = k[0, 0].float().cpu().double().numpy()
-    vs = v[0, 0].float().cpu().double().numpy()
+    qs, ks, vs = (t[0, 0].float().cpu().double().numpy() for t in (prob.q, prob.k, prob.v))
+    perm_np = prob.perm_np
     if perm_np is not None:
         qs, ks, vs = qs[perm_np], ks[perm_np], vs[perm_np]
-    # ~10 s of oracle work on the GPU box's host: 128 query blocks at 32K
-    # (8.4 s measured for 96), scaled by 1/N
-    qb = sample_qblocks(tm, n=max(8, int(128 * 32768 / N)))
+    qb = list(range(tm)) if N <= 32768 else sample_qblocks(tm, n=max(8, int(256 * 32768 / N)))
     t0 = time.perf_counter()
-    o_ref, M, near, cnt, _ = O.spargeattn_head(qs, ks, vs, O.f32(cfg["tau"]), O.f32(cfg["theta"]),
-                                               O.f32(cfg["lam"]), causal=cfg["causal"],
-                                               qblocks=qb)
+    o_ref, M, near, cnt, _, used = spargeattn_head_parallel(
+        qs, ks, vs, O.f32(cfg["tau"]), O.f32(cfg["theta"]), O.f32(cfg["lam"]),
+        causal=cfg["causal"], qblocks=qb)
     secs = time.perf_counter() - t0
     rows = np.concatenate([np.arange(i * 128, min((i + 1) * 128, N)) for i in qb])
     og = snap[0].double().numpy()
     if perm_np is not None:
         og = og[perm_np]                  # GPU O back to permuted order
-    l1 = float(np.abs(og[rows] - o_ref[rows]).sum() / np.abs(o_ref[rows]).sum())
-    dense_rows = O.dense_attention(qs, ks, vs, causal=cfg["causal"], rows=rows)
-    l1_dense = float(np.abs(og[rows] - dense_rows).sum() / np.abs(dense_rows).sum())
+    a, b = og[rows], o_ref[rows]
+    l1 = float(np.abs(a - b).sum() / np.abs(b).sum())
+    worst_row = float((np.abs(a - b).sum(1) / np.abs(b).sum(1)).max())
+    drows = rows[np.linspace(0, len(rows) - 1, min(len(rows), 512)).astype(int)]
+    dense_rows = O.dense_attention(qs, ks, vs, causal=cfg["causal"], rows=drows)
+    l1_dense = float(np.abs(og[drows] - dense_rows).sum() / np.abs(dense_rows).sum())
     gm = snap[1].numpy()
     mism = gm != M
     ops = sample_dense_ops(cfg, qb)
-    _ = group
+    rate = ops / secs
     return {
-        "cpu_baseline": {"value": ops / secs / 1e12, "unit": "TOPS", "cores": oracle_threads(),
-                         "kind": "oracle", "seconds": secs,
+        "cpu_baseline": {"value": rate / 1e12, "unit": "TOPS", "cores": used, "kind": "oracle",
+                         "host_cores": cores(), "seconds": secs,
+                         "extrapolated_full_seconds": ops_total / rate,
+                         "extrapolated_note": "EXTRAPOLATED: whole-job dense ops / the sample's "
+                                              "measured rate (not run)",
                          "sample": f"q-head 0: full stage-1 prediction + sparse loop on "
-                                   f"q-blocks {qb} ({len(rows)} of {N} rows)"},
-        "parity": {"l1_vs_oracle": l1, "l1_vs_dense": l1_dense,
+                                   f"{len(qb)} of {tm} q-blocks ({len(rows)} of {N} rows), "
+                                   f"{used} worker processes"},
+        "parity": {"l1_vs_oracle": l1, "worst_row_l1_vs_oracle": worst_row,
+                   "l1_vs_oracle_dense_rows": l1_dense, "dense_rows": int(len(drows)),
                    "mask_mismatch": int(mism.sum()),
                    "mask_mismatch_outside_near": int((mism & ~near).sum()),
-                   "near_threshold": int(near.sum()), "head": 0, "rows": int(len(rows))},
+                   "near_threshold": int(near.sum()), "head": 0, "rows": int(len(rows)),
+                   "qk_tiles_oracle": cnt["qk"], "pv_slices_oracle": cnt["pv_slices"]},
     }
 
 
@@ -502,13 +735,15 @@ def emit(result, rank, args):
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
-    """The oracle as it stands on the host cores (the tier's reference arm).
-    Under torchrun only rank 0 runs; the others exit 0 without work."""
+    """The oracle as it stands on the host cores (the tier's reference arm),
+    fanned out over the cores (oracle/parallel.py).  Under torchrun only
+    rank 0 runs; the others exit 0 without work."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle as O
-    cfg = workload_cfg(args.workload)
+    from oracle.parallel import cores, spargeattn_head_parallel
+    cfg = hyper(workload_cfg(args.workload), args.workload, args.triple)
     for key in ("tau", "theta", "lam"):
         if getattr(args, key) is not None:
             cfg[key] = getattr(args, key)
@@ -521,12 +756,14 @@ def run_reference(args):
     if perm is not None:
         qs, ks, vs = qs[perm], ks[perm], vs[perm]
     rng = np.random.default_rng(0)
+    ncores = cores()
     times, ops = [], []
+    used = 1
     for s in range(args.warmup + args.steps):
-        qb = sorted(rng.choice(tm, size=min(2, tm), replace=False).tolist())
+        qb = sorted(rng.choice(tm, size=min(ncores, tm), replace=False).tolist())
         t0 = time.perf_counter()
-        O.spargeattn_head(qs, ks, vs, O.f32(cfg["tau"]), O.f32(cfg["theta"]), O.f32(cfg["lam"]),
-                          causal=cfg["causal"], qblocks=qb)
+        *_, used = spargeattn_head_parallel(qs, ks, vs, O.f32(cfg["tau"]), O.f32(cfg["theta"]),
+                                            O.f32(cfg["lam"]), causal=cfg["causal"], qblocks=qb)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
@@ -536,15 +773,15 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.workload, "N": N, "d": d, "Hq": cfg["Hq"],
                    "Hkv": cfg["Hkv"], "causal": bool(cfg["causal"]), "tau": cfg["tau"],
-                   "theta": cfg["theta"], "lambda": cfg["lam"]},
-        "cpu_baseline": {"value": value, "unit": "TOPS", "cores": oracle_threads(),
-                         "kind": "oracle",
-                         "sample": "per step: q-head 0 full stage-1 prediction + sparse loop "
-                                   "on 2 random q-blocks"},
+                   "theta": cfg["theta"], "lambda": cfg["lam"], "triple": cfg["triple"]},
+        "cpu_baseline": {"value": value, "unit": "TOPS", "cores": used, "kind": "oracle",
+                         "sample": f"per step: q-head 0 full stage-1 prediction + sparse loop "
+                                   f"on {min(ncores, tm)} random q-blocks over {used} worker "
+                                   f"processes"},
         "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

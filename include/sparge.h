@@ -44,6 +44,8 @@ enum sparge_status {
 };
 
 enum sparge_dtype { SPARGE_BF16 = 0, SPARGE_FP16 = 1 };
+/* largest T_n = ceil(N / bk) sparge_predict_mask accepts (N <= 2^20) */
+enum { SPARGE_MAX_TN = 16384 };
 /* Operand type of the P~V product (Alg. 1 line 16):
  *   SPARGE_PV_SAME_AS_INPUT  P~ rounded to in_dtype, V in in_dtype (R12);
  *   SPARGE_PV_FP8_E4M3       scope row f4 (SageAttention2-style, footnote
@@ -174,7 +176,8 @@ int sparge_quantize_smooth_k(const sparge_shape* shape, const void* k, sparge_st
  *   workspace/ws_bytes  >= sparge_predict_workspace(shape), 256-byte aligned
  *         (scratch for S^; contents undefined on return)
  * tau in (0, 1], theta in [-1, 1] (float32, compared in fp64).
- * Errors: SPARGE_EINVAL (range / NULL / T_n > 2048, i.e. N > 131072),
+ * Errors: SPARGE_EINVAL (range / NULL / T_n > SPARGE_MAX_TN, i.e.
+ * N > 1048576: one compressed-map row is held per warp in shared memory),
  * SPARGE_ECUDA.
  */
 int sparge_predict_mask(const sparge_shape* shape,

@@ -18,8 +18,7 @@
 //               8-row strip per warp; written to the workspace.
 // k_topcdf_rows one warp per (head, query block): masks, softmax, the
 //               sort-free binned TopCdf selection (topcdf_binned: fixed-point
-//               integer bin masses, only the boundary bin sorted; the full
-//               bitonic sorts remain behind SPARGE_TOPCDF_BINNED=0), forcing,
+//               integer bin masses, only the boundary bin sorted), forcing,
 //               causal AND + guard, ballot compaction into the LUT.
 #include <cstdint>
 #include <cfloat>
@@ -54,12 +53,16 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 template <int D>
 __global__ void __launch_bounds__(kGemmThreads)
 k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_pooled,
-            int Hq, int Hkv, int T_m, int T_n, double* __restrict__ shat) {
+            int Hq, int Hkv, int T_m, int T_n, int N, int bq, int bk, int causal,
+            double* __restrict__ shat) {
   constexpr int KR = D + 4;         // padded row (doubles): KR % 16 == 4
   extern __shared__ __align__(16) unsigned char smem[];
   double* sq = reinterpret_cast<double*>(smem);          // [kTile][KR]
   double* sk = sq + kTile * KR;                          // [kTile][KR]
   const int j0 = blockIdx.x * kTile, i0 = blockIdx.y * kTile, bhq = blockIdx.z;
+  // causal: a tile whose every key block is dead for every query block of
+  // the tile (R8-i) is never read by k_topcdf_rows -- skip it
+  if (causal && j0 * bk > min((min(i0 + kTile, T_m)) * bq, N) - 1) return;
   const int hq = bhq % Hq, b = bhq / Hq;
   const int hkv = hq / (Hq / Hkv);
   const int64_t qbase = static_cast<int64_t>(bhq) * T_m;
@@ -116,7 +119,24 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
 }
 
 // ---------------------------------------------------------------- TopCdf rows
-constexpr int kRowWarps = 4;
+// k_topcdf_rows: up to kMaxRowWarps rows (one warp each) per CTA, each warp
+// holding its row in shared memory: pow2ceil(T_n) 64-bit keys (the boundary
+// bin is sorted in place by a power-of-two bitonic sort), T_n flags and the
+// bin sums.  T_n <= kMaxTn (N <= 2^20 tokens) keeps one row within a CTA's
+// shared memory; the key's low kIdxBits mantissa bits carry the index.
+constexpr int kMaxRowWarps = 4;
+constexpr int kIdxBits = 16;
+constexpr uint64_t kIdxMask = (1ull << kIdxBits) - 1;
+constexpr size_t kRowSmemMax = 200 * 1024;
+constexpr int kNB = 256;
+__host__ __device__ inline int pow2ceil(int n) {
+  int p = 32;
+  while (p < n) p <<= 1;
+  return p;
+}
+__host__ __device__ inline size_t row_smem_bytes(int T_n) {
+  return static_cast<size_t>(pow2ceil(T_n)) * 8 + kNB * 8 + ((T_n + 15) / 16) * 16;
+}
 
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
@@ -128,42 +148,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double t = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += t;
-  }
-  return v;
-}
-
-// Warp-synchronous bitonic sort, descending, of SORTN 64-bit keys in shared
-// memory; branch-free compare-exchange, unrolled per stage.
-template <int SORTN>
-__device__ __forceinline__ void sort_desc(uint64_t* key, int lane) {
-#pragma unroll 1
-  for (int k = 2; k <= SORTN; k <<= 1) {
-#pragma unroll 1
-    for (int jj = k >> 1; jj > 0; jj >>= 1) {
-#pragma unroll
-      for (int u = 0; u < (SORTN / 2 + 31) / 32; ++u) {
-        const int t = lane + 32 * u;
-        if (SORTN >= 64 || t < SORTN / 2) {
-          // pair (a, a + jj): a = 2*jj*(t / jj) + t % jj, jj a power of two
-          const int a = t + (t & ~(jj - 1));
-          const int c = a + jj;
-          const uint64_t ka = key[a], kc = key[c];
-          const bool desc_block = (a & k) == 0;
-          const bool sw = desc_block ? (kc > ka) : (ka > kc);
-          key[a] = sw ? kc : ka;
-          key[c] = sw ? ka : kc;
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
 // Warp-synchronous bitonic sort, descending, of n (a power of two) 64-bit
 // keys in shared memory, runtime n.
 __device__ __forceinline__ void sort_desc_n(uint64_t* key, int n, int lane) {
@@ -190,10 +174,11 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 }
 
 // TopCdf selection without a full sort (v4).  Keys as in the sort path
-// (truncated P^ bits | 2047 - j).  The selected set is a prefix of the
+// (truncated P^ bits | kIdxMask - j).  The selected set is a prefix of the
 // descending order, so only the entries of the BOUNDARY bin need ordering:
 //   * P^ is put in fixed point, q_j = floor(p_j * 2^s) with p_max * 2^s in
-//     [2^52, 2^53) (sum < 2^64): integer sums are exact and order-free, so
+//     [2^52, 2^53) or s = 63 (sum <= 2^63 (1 + eps) < 2^64 as P^ sums to
+//     1): integer sums are exact and order-free, so
 //     the result is deterministic and equals the sequential fp64 cumsum up
 //     to ~2^-52 relative (inside the 1e-6 near-threshold band);
 //   * bins by (binade below the max, top 3 mantissa bits): NB = 256 bins in
@@ -202,20 +187,18 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 //     tau * total; bins before it are selected, bins after it are not, and
 //     the entries of b* are sorted and scanned from the mass above it.
 // tau >= 1 selects everything (c_k <= c_last for every k, R4).  Rank 0 is
-// always selected (guard).  ukey: the keys, entry j at kix(j) (padded when
-// PAD), overwritten: the boundary bin is compacted in place to ukey[0, m)
-// and sorted there; bins: scratch of NB counts + NB sums; flag: [T_n].
-constexpr int kNB = 256;
+// always selected (guard).  ukey: the keys, entry j at ukey[j] (room for
+// pow2ceil(T_n) keys), overwritten: the boundary bin is compacted in place to
+// ukey[0, m) and sorted there; bsum: NB bin sums; flag: [T_n].
 __device__ __forceinline__ int bin_of(uint64_t key, int emax) {
   const int e = static_cast<int>(key >> 52) & 0x7FF;
   const int db = emax - e;
   if (db >= kNB / 8) return kNB - 1;
   return db * 8 + (7 - static_cast<int>((key >> 49) & 7u));
 }
-template <bool PAD>
-__device__ void topcdf_binned(uint64_t* ukey, unsigned int* bcnt, unsigned long long* bsum,
-                              uint8_t* flag, int T_n, double tau, int lane) {
-  auto kix = [](int j) { return PAD ? j + (j >> 5) : j; };
+__device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t* flag, int T_n,
+                              double tau, int lane) {
+  auto kix = [](int j) { return j; };
   uint64_t* list = ukey;
   // max key -> its exponent; fixed-point scale
   uint64_t kmax = 0;
@@ -223,14 +206,15 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned int* bcnt, unsigned long 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
   const int emax = static_cast<int>(kmax >> 52) & 0x7FF;
-  const int sc = 52 - (emax - 1023);
+  // scale so that max q_j is in [2^52, 2^53) -- capped at 2^63 so the sum
+  // (P^ sums to 1) stays below 2^64 when T_n > 2^11 (p_max may be < 2^-11)
+  const int sc = min(52 - (emax - 1023), 63);
   for (int b = lane; b < kNB; b += 32) bsum[b] = 0ull;
-  (void)bcnt;
   __syncwarp();
   unsigned long long part = 0;
   for (int j = lane; j < T_n; j += 32) {
     const uint64_t k = ukey[kix(j)];
-    const unsigned long long qj = __double2ull_rz(ldexp(__longlong_as_double(k & ~0x7FFull), sc));
+    const unsigned long long qj = __double2ull_rz(ldexp(__longlong_as_double(k & ~kIdxMask), sc));
     const int b = bin_of(k, emax);
     atomicAdd(&bsum[b], qj);
     part += qj;
@@ -292,258 +276,96 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned int* bcnt, unsigned long 
       const int t = t0 + lane;
       const uint64_t k = (t < m) ? list[t] : 0ull;
       unsigned long long qv =
-          (t < m) ? __double2ull_rz(ldexp(__longlong_as_double(k & ~0x7FFull), sc)) : 0ull;
+          (t < m) ? __double2ull_rz(ldexp(__longlong_as_double(k & ~kIdxMask), sc)) : 0ull;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long y = __shfl_up_sync(0xffffffffu, qv, o);
         if (lane >= o) qv += y;
       }
       const unsigned long long c = carry + qv;
-      if (t < m) flag[2047 - static_cast<int>(k & 0x7FFull)] = (static_cast<double>(c) <= thr) ? 1 : 0;
+      if (t < m) flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (static_cast<double>(c) <= thr) ? 1 : 0;
       carry = __shfl_sync(0xffffffffu, c, 31);
     }
   }
   __syncwarp();
   // guard: the top entry
-  if (lane == 0) flag[2047 - static_cast<int>(kmax & 0x7FFull)] = 1;
+  if (lane == 0) flag[kIdxMask - static_cast<int>(kmax & kIdxMask)] = 1;
   __syncwarp();
 }
 
-// Register bitonic sort, descending, of SORTN = 32*R 64-bit keys held
-// lane-major (rank i = lane*R + r): stages with partner distance jj < R are
-// compare-exchanges between two registers of one lane, stages with jj >= R
-// exchange register r with lane ^ (jj/R) by shuffle (15 of the 55 stages at
-// SORTN = 1024).  No shared memory, no bank conflicts.
-template <int R, int JJ>
-__device__ __forceinline__ void reg_stage_c(uint64_t (&v)[R], int k, int lane) {
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    if ((r & JJ) == 0) {
-      const int i = lane * R + r;
-      const bool desc = (i & k) == 0;
-      const uint64_t a = v[r], b = v[r + JJ];
-      const bool sw = desc ? (b > a) : (a > b);
-      v[r] = sw ? b : a;
-      v[r + JJ] = sw ? a : b;
-    }
-  }
-}
-template <int R>
-__device__ __forceinline__ void reg_stage(uint64_t (&v)[R], int jj, int k, int lane) {
-  if (R > 1 && jj == 1) reg_stage_c<R, (R > 1 ? 1 : 0)>(v, k, lane);
-  if (R > 2 && jj == 2) reg_stage_c<R, (R > 2 ? 2 : 0)>(v, k, lane);
-  if (R > 4 && jj == 4) reg_stage_c<R, (R > 4 ? 4 : 0)>(v, k, lane);
-  if (R > 8 && jj == 8) reg_stage_c<R, (R > 8 ? 8 : 0)>(v, k, lane);
-  if (R > 16 && jj == 16) reg_stage_c<R, (R > 16 ? 16 : 0)>(v, k, lane);
-}
-template <int R>
-__device__ __forceinline__ void lane_stage(uint64_t (&v)[R], int ld, int k, int lane) {
-  const bool lower = (lane & ld) == 0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], ld);
-    const bool desc = ((lane * R + r) & k) == 0;
-    const bool take_max = (lower == desc);
-    const bool o_bigger = o > v[r];
-    v[r] = (take_max == o_bigger) ? o : v[r];
-  }
-}
-template <int R>
-__device__ __forceinline__ void sort_desc_reg(uint64_t (&v)[R], int lane) {
-#pragma unroll 1
-  for (int k = 2; k <= 32 * R; k <<= 1) {
-#pragma unroll 1
-    for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      if (jj >= R) lane_stage<R>(v, jj / R, k, lane);
-      else reg_stage<R>(v, jj, k, lane);
-    }
-  }
-}
-
-// padded shared-memory index of entry j (one 8-B pad per 32 entries) so the
-// lane-major reads lane*R + r hit distinct banks
-__device__ __forceinline__ int pidx(int j) { return j + (j >> 5); }
-
-// TopCdf of one row with the register sort: keys (padded layout) in smem ->
-// registers (lane-major), sort, lane-local sequential prefix sums + a warp
-// scan of the lane totals, flags by rank.
-template <int R>
-__device__ __forceinline__ void topcdf_reg(uint64_t* ukey, uint8_t* flag, int T_n, double tau,
-                                           int lane) {
-  uint64_t v[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = ukey[pidx(lane * R + r)];
-  sort_desc_reg<R>(v, lane);
-  // c_k = (exclusive prefix of the lane totals) + lane-local sequential sum;
-  // recomputed identically in each pass (deterministic), so no array of c
-  auto p_of = [&](int r) {
-    return (lane * R + r < T_n) ? __longlong_as_double(v[r] & ~0x7FFull) : 0.0;
-  };
-  double tot = 0.0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) tot += p_of(r);
-  const double off = warp_incl_scan(tot, lane) - tot;
-  double acc = off, cmax = 0.0;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    acc += p_of(r);
-    cmax = fmax(cmax, acc);
-  }
-  const double thr = tau * warp_max(cmax);
-  acc = off;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    acc += p_of(r);
-    const int k = lane * R + r;
-    if (k < T_n) flag[2047 - static_cast<int>(v[r] & 0x7FFull)] = (acc <= thr || k == 0) ? 1 : 0;
-  }
-  __syncwarp();
-}
-
-// RS = SORTN / 32 for the register sort (SORTN <= 1024), 0 = the
-// shared-memory sort (SORTN = 2048).  SPARGE_TOPCDF_BINNED (default): the
-// sort-free binned selection above instead of either sort.
-#ifndef SPARGE_TOPCDF_BINNED
-#define SPARGE_TOPCDF_BINNED 1
-#endif
-constexpr bool kBinned = SPARGE_TOPCDF_BINNED != 0;
-#ifndef SPARGE_TOPCDF_MINB32
-#define SPARGE_TOPCDF_MINB32 3
-#endif
-template <int RS>
-__global__ void __launch_bounds__(kRowWarps * 32, RS >= 32 ? SPARGE_TOPCDF_MINB32 : 4)
+template <int D>
+__global__ void __launch_bounds__(kMaxRowWarps * 32)
 k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
               const double* __restrict__ k_sim, int Hq, int Hkv, int N, int T_m, int T_n,
-              int rows_total, int sortn, int bq, int bk, int causal, double tau, double theta,
+              int rows_total, int bq, int bk, int causal, double tau, double theta,
               uint8_t* __restrict__ mask, int32_t* __restrict__ lut, int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int row = blockIdx.x * kRowWarps + wid;          // (b*Hq + hq)*T_m + i
+  const int row_warps = blockDim.x >> 5;
+  const int row = blockIdx.x * row_warps + wid;          // (b*Hq + hq)*T_m + i
   if (row >= rows_total) return;
-  const int kstride = sortn + sortn / 32;                 // padded key slots per warp
-  uint64_t* ukey = reinterpret_cast<uint64_t*>(smem) + wid * kstride;
+  // per warp: T_n keys (8 B), T_n flags, kNB bin sums (8 B)
+  const size_t per_warp = row_smem_bytes(T_n);
+  unsigned char* base_w = smem + wid * per_warp;
+  uint64_t* ukey = reinterpret_cast<uint64_t*>(base_w);
   double* key = reinterpret_cast<double*>(ukey);
-  uint8_t* flag = smem + static_cast<size_t>(kRowWarps) * kstride * 8 + wid * sortn;
-  // binned selection scratch: NB bin sums + NB bin counts per warp
-  unsigned long long* bsum = reinterpret_cast<unsigned long long*>(
-      smem + static_cast<size_t>(kRowWarps) * (kstride * 8 + sortn)) + wid * kNB;
-  unsigned int* bcnt = reinterpret_cast<unsigned int*>(bsum + (kRowWarps - wid) * kNB) + wid * kNB;
+  unsigned long long* bsum = reinterpret_cast<unsigned long long*>(base_w + static_cast<size_t>(T_n) * 8);
+  uint8_t* flag = base_w + static_cast<size_t>(T_n) * 8 + kNB * 8;
 
   const int i = row % T_m, bhq = row / T_m;
   const int hq = bhq % Hq, b = bhq / Hq;
   const int64_t kbase = (static_cast<int64_t>(b) * Hkv + hq / (Hq / Hkv)) * T_n;
   const int last_q = min((i + 1) * bq, N) - 1;
+  // causal: key blocks j >= n_live are dead for this row (R8-i) -- never
+  // loaded (k_shat_dmma does not compute tiles that are dead for a whole CTA)
+  const int n_live = causal ? min(T_n, last_q / bk + 1) : T_n;
   const double* srow = shat + static_cast<int64_t>(row) * T_n;
 
   // ---- S^ row with the -inf columns (fixed K blocks, causally dead) ----
-  // (register-sort rows keep entry j at the padded slot pidx(j) throughout)
-  constexpr bool padded = RS > 0;
-  auto kix = [&](int j) { return padded ? pidx(j) : j; };
-  double mx = -INFINITY;
-#ifdef SPARGE_TOPCDF_SERIAL_LOADS
-  for (int j = lane; j < T_n; j += 32) {
-    const bool dead = causal && (j * bk > last_q);
-    const double s = (dead || k_sim[kbase + j] < theta) ? -INFINITY : srow[j];
-    key[kix(j)] = s;
-    mx = fmax(mx, s);
-  }
-#else
   // the row's global loads batched kLoadBatch deep (the smem stores between
   // them would otherwise serialise one load latency per 32 entries)
   constexpr int kLoadBatch = 8;
+  double mx = -INFINITY;
   for (int j0 = lane; j0 < T_n; j0 += 32 * kLoadBatch) {
     double sv[kLoadBatch], kv[kLoadBatch];
 #pragma unroll
     for (int u = 0; u < kLoadBatch; ++u) {
       const int j = j0 + 32 * u;
-      sv[u] = (j < T_n) ? __ldg(srow + j) : 0.0;
-      kv[u] = (j < T_n) ? __ldg(k_sim + kbase + j) : 0.0;
+      sv[u] = (j < n_live) ? __ldg(srow + j) : -INFINITY;
+      kv[u] = (j < n_live) ? __ldg(k_sim + kbase + j) : 1.0;
     }
 #pragma unroll
     for (int u = 0; u < kLoadBatch; ++u) {
       const int j = j0 + 32 * u;
       if (j < T_n) {
-        const bool dead = causal && (j * bk > last_q);
-        const double s = (dead || kv[u] < theta) ? -INFINITY : sv[u];
-        key[kix(j)] = s;
+        const double s = (kv[u] < theta) ? -INFINITY : sv[u];
+        key[j] = s;
         mx = fmax(mx, s);
       }
     }
   }
-#endif
   mx = warp_max(mx);
   const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
 
   if (!flagged) {
     double part = 0.0;
     for (int j = lane; j < T_n; j += 32) {
-      const double kv = key[kix(j)];
+      const double kv = key[j];
       const double e = (kv == -INFINITY) ? 0.0 : exp(kv - mx);
-      key[kix(j)] = e;
+      key[j] = e;
       part += e;
     }
     const double total = warp_sum(part);
     // One 64-bit sort key per entry: the bits of P^ (>= 0, so integer order =
-    // value order) with the low 11 mantissa bits replaced by 2047 - j.  Sorting
-    // the keys descending orders (P^ desc, j asc) up to a 2^-42 relative
-    // truncation of P^ -- far inside the 1e-6 near-threshold band of the
-    // parity criterion; the cumulative sum uses the truncated values.
-    // Padding keys are 0 and sort last (a real entry has key >= 2047 - j > 0).
-    if (kBinned) {
-      for (int j = lane; j < T_n; j += 32) {
-        const int pj = kix(j);
-        ukey[pj] = (static_cast<uint64_t>(__double_as_longlong(key[pj] / total)) & ~0x7FFull) |
-                   static_cast<uint64_t>(2047 - j);
-      }
-      __syncwarp();
-      topcdf_binned<padded>(ukey, bcnt, bsum, flag, T_n, tau, lane);
-    } else if (RS > 0) {
-      // register sort: composite keys in place at the padded positions,
-      // read back lane-major
-      for (int j = lane; j < sortn; j += 32) {
-        const int pj = pidx(j);
-        ukey[pj] = (j < T_n)
-                       ? ((static_cast<uint64_t>(__double_as_longlong(key[pj] / total)) & ~0x7FFull) |
-                          static_cast<uint64_t>(2047 - j))
-                       : 0ull;
-      }
-      __syncwarp();
-      topcdf_reg<(RS > 0 ? RS : 1)>(ukey, flag, T_n, tau, lane);
-    } else {
-    for (int j = lane; j < sortn; j += 32) {
-      ukey[j] = (j < T_n)
-                    ? ((static_cast<uint64_t>(__double_as_longlong(key[j] / total)) & ~0x7FFull) |
-                       static_cast<uint64_t>(2047 - j))
-                    : 0ull;
-    }
+    // value order) with the low kIdxBits mantissa bits replaced by kIdxMask - j.
+    // Ordering the keys descending orders (P^ desc, j asc) up to a 2^-36
+    // relative truncation of P^ -- far inside the 1e-6 near-threshold band of
+    // the parity criterion; the cumulative sums use the truncated values.
+    for (int j = lane; j < T_n; j += 32)
+      ukey[j] = (static_cast<uint64_t>(__double_as_longlong(key[j] / total)) & ~kIdxMask) |
+                static_cast<uint64_t>(kIdxMask - j);
     __syncwarp();
-    sort_desc<2048>(ukey, lane);
-    // inclusive cumulative sum in rank order, 32 ranks per step (rank
-    // 32*s + lane): conflict-free shared-memory reads.  Pass 1 finds c_last,
-    // pass 2 recomputes the identical prefix sums and decides.  c_last (R4)
-    // is the maximum of the computed prefix sums: equal to the last one in
-    // exact arithmetic, and it keeps tau = 1 exact under rounding.
-    const int steps = (T_n + 31) / 32;
-    double carry = 0.0, cmax = 0.0;
-    for (int s = 0; s < steps; ++s) {
-      const int k = 32 * s + lane;
-      const double p = (k < T_n) ? __longlong_as_double(ukey[k] & ~0x7FFull) : 0.0;
-      const double c = carry + warp_incl_scan(p, lane);
-      cmax = fmax(cmax, c);
-      carry = __shfl_sync(0xffffffffu, c, 31);
-    }
-    const double thr = tau * warp_max(cmax);
-    carry = 0.0;
-    for (int s = 0; s < steps; ++s) {
-      const int k = 32 * s + lane;
-      const uint64_t kv = (k < T_n) ? ukey[k] : 0ull;
-      const double p = (k < T_n) ? __longlong_as_double(kv & ~0x7FFull) : 0.0;
-      const double c = carry + warp_incl_scan(p, lane);
-      carry = __shfl_sync(0xffffffffu, c, 31);
-      if (k < T_n) flag[2047 - static_cast<int>(kv & 0x7FFull)] = (c <= thr || k == 0) ? 1 : 0;
-    }
-    __syncwarp();
-    }
+    topcdf_binned(ukey, bsum, flag, T_n, tau, lane);
   }
 
   // ---- forcing (Eq. 5), flagged rows, causal live AND + diagonal guard ----
@@ -557,9 +379,9 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
     bool f = false;
     if (j < T_n) {
       f = flagged ? true : (flag[j] != 0);
-      if (row_fix || k_sim[kbase + j] < theta) f = true;
+      if (row_fix || (j < n_live && k_sim[kbase + j] < theta)) f = true;
       if (causal) {
-        if (j * bk > last_q) f = false;
+        if (j >= n_live) f = false;
         if (j == guard) f = true;
       }
       if (mrow) mrow[j] = f ? 1 : 0;
@@ -584,29 +406,20 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
   if (e != cudaSuccess) return e;
   dim3 g1((T_n + kTile - 1) / kTile, (T_m + kTile - 1) / kTile, s.B * s.Hq);
   k_shat_dmma<D><<<g1, kGemmThreads, smem_g, stream>>>(q_pooled, k_pooled, s.Hq, s.Hkv, T_m, T_n,
-                                                        shat);
-  int sortn = 32;
-  while (sortn < T_n) sortn <<= 1;
-  const size_t smem_r = static_cast<size_t>(kRowWarps) * ((sortn + sortn / 32) * 8 + sortn + kNB * 12);
+                                                        s.N, s.bq, s.bk, s.causal, shat);
+  // rows per CTA: up to kMaxRowWarps, as many as fit the shared memory
+  const size_t per_warp = row_smem_bytes(T_n);
+  const int warps = static_cast<int>(std::min<size_t>(kMaxRowWarps, kRowSmemMax / per_warp));
+  if (warps < 1) return cudaErrorInvalidValue;
+  const size_t smem_r = per_warp * warps;
   const int rows = s.B * s.Hq * T_m;
-  auto run = [&](auto kern) -> cudaError_t {
-    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(smem_r));
-    if (e2 != cudaSuccess) return e2;
-    kern<<<(rows + kRowWarps - 1) / kRowWarps, kRowWarps * 32, smem_r, stream>>>(
-        shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, sortn, s.bq, s.bk, s.causal,
-        static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
-    return cudaGetLastError();
-  };
-  switch (sortn) {
-    case 32: return run(k_topcdf_rows<1>);
-    case 64: return run(k_topcdf_rows<2>);
-    case 128: return run(k_topcdf_rows<4>);
-    case 256: return run(k_topcdf_rows<8>);
-    case 512: return run(k_topcdf_rows<16>);
-    case 1024: return run(k_topcdf_rows<32>);
-    default: return run(k_topcdf_rows<0>);
-  }
+  e = cudaFuncSetAttribute(k_topcdf_rows<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem_r));
+  if (e != cudaSuccess) return e;
+  k_topcdf_rows<D><<<(rows + warps - 1) / warps, warps * 32, smem_r, stream>>>(
+      shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, s.bq, s.bk, s.causal,
+      static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
+  return cudaGetLastError();
 }
 
 }  // namespace

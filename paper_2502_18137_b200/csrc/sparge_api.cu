@@ -184,7 +184,7 @@ int sparge_predict_mask(const sparge_shape* shape, const double* q_pooled, const
   if (!(tau > 0.f && tau <= 1.f)) return SPARGE_EINVAL;
   if (!(theta >= -1.f && theta <= 1.f)) return SPARGE_EINVAL;
   const int T_n = (shape->N + shape->bk - 1) / shape->bk;
-  if (T_n > 2048) return SPARGE_EINVAL;   // one shared-memory row of 2048 (N <= 131072)
+  if (T_n > SPARGE_MAX_TN) return SPARGE_EINVAL;   // one compressed-map row per warp in smem
   cudaError_t e = launch_predict(*shape, q_pooled, q_sim, k_pooled, k_sim, tau, theta, mask, lut,
                                  cnt, workspace, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;

@@ -100,3 +100,18 @@ def test_python_binding_validates_inputs(sp):
         sp._validate(q4, q4[:, :3], q4[:, :3], None, None, False)
     with pytest.raises(ValueError, match="out"):
         sp._validate(q4, q4[:, :2], q4[:, :2], q4[:, :1], None, False)
+
+
+def test_predict_rejects_rows_longer_than_max_tn(sp):
+    """T_n = ceil(N / 64) above SPARGE_MAX_TN = 16384 (N > 2^20) is rejected
+    before any launch (one compressed-map row per warp in shared memory)."""
+    fake = ctypes.c_void_p(1 << 20)                       # 256-B aligned, never touched
+    for N, ok in ((1 << 20, True), ((1 << 20) + 1, False)):
+        shape = sp.make_shape(1, 1, 1, N, 128)
+        ws = sp._lib.sparge_predict_workspace(ctypes.byref(shape))
+        assert ws > 0
+        if ok:
+            continue                                      # a valid call would launch
+        rc = sp._lib.sparge_predict_mask(ctypes.byref(shape), fake, fake, fake, fake, 0.9, 0.5,
+                                         None, fake, fake, fake, ws, None)
+        assert rc == sp.SPARGE_EINVAL

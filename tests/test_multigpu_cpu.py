@@ -93,3 +93,27 @@ def test_head_sharded_gather_equals_single_process(tmp_path, Hq, Hkv):
     ref = np.stack([O.spargeattn_head(q[h], k[h // grp], v[h // grp], 0.9, 0.5, -5.0,
                                       causal=True)[0] for h in range(Hq)])
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("kind", ["llm_rope", "llm_local", "video"])
+def test_head_shard_inputs_equal_slices_of_full(kind):
+    """Each rank generates only its heads from per-global-head seeds
+    (nothing is sent); the shard must equal the same slice of
+    the single-GPU input, so gathered O can equal the single-GPU O bit for
+    bit."""
+    import bench
+    from paper_2502_18137_b200 import multigpu
+    if kind == "video":
+        cfg = dict(kind="video", T=2, H=4, W=6, text_prefix=5, d=64, Hq=6, Hkv=6)
+        cfg["N"] = 5 + 2 * 4 * 6
+    else:
+        cfg = dict(kind=kind, N=300, d=64, Hq=8, Hkv=2)
+    q, k, v = bench.gen_inputs(cfg, 1000)
+    for world in (2, 4):
+        for rank in range(world):
+            hq, hkv = multigpu.local_heads(cfg["Hq"], cfg["Hkv"], world, rank)
+            if not hq:
+                continue
+            qs, ks, vs = bench.gen_inputs(cfg, 1000, heads=hq)
+            assert np.array_equal(qs, q[:, hq]) and np.array_equal(ks, k[:, hkv])
+            assert np.array_equal(vs, v[:, hkv])
