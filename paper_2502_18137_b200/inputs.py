@@ -115,65 +115,115 @@ def llm_local(seed, N, d=128, Hq=32, Hkv=8, B=1, gamma=0.7, noise=0.6, rho=0.998
     return q, k, v
 
 
-def rope(x, base=500000.0, pos=None):
+_ROPE_CACHE = {}
+
+
+def _rope_table(n, d, base):
+    key = (n, d, base)
+    if key not in _ROPE_CACHE:
+        w = base ** (-np.arange(d // 2) * 2.0 / d)
+        ang = np.arange(n, dtype=np.float64)[:, None] * w[None, :]
+        _ROPE_CACHE.clear()                      # one shape at a time
+        _ROPE_CACHE[key] = (np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32))
+    return _ROPE_CACHE[key]
+
+
+def rope(x, base=500000.0):
     """Rotary position embedding of rows x [N, d] at positions 0..N-1 (the
     Llama rotate-half convention: pair (c, c + d/2) rotated by t * w_c,
-    w_c = base^(-2c/d)).  Input synthesis only -- the method under test never
-    sees positions."""
+    w_c = base^(-2c/d)), in float32.  Input synthesis only -- the method
+    under test never sees positions."""
     n, d = x.shape
     h = d // 2
-    w = base ** (-np.arange(h) * 2.0 / d)
-    ang = (np.arange(n, dtype=np.float64) if pos is None else pos)[:, None] * w[None, :]
-    c, s_ = np.cos(ang), np.sin(ang)
+    c, s_ = _rope_table(n, d, base)
     x1, x2 = x[:, :h], x[:, h:]
     return np.concatenate([x1 * c - x2 * s_, x1 * s_ + x2 * c], 1)
 
 
+def _ar1_coarse(g, n, width, rho, stride=8):
+    """The AR(1) latent sampled every `stride` tokens (AR coefficient
+    rho^stride) and linearly interpolated, float32: with rho = 0.998 the
+    correlation length is ~500 tokens, so the latent is smooth on the
+    interpolation scale (generation speed at 128K tokens)."""
+    from scipy.signal import lfilter
+    m = (n + stride - 1) // stride + 1
+    r = rho ** stride
+    eps = g.standard_normal((m, width), dtype=np.float32)
+    eps[0] /= math.sqrt(1 - r * r)
+    zc = lfilter(np.float32([math.sqrt(1 - r * r)]), np.float32([1.0, -r]), eps, axis=0)
+    t = np.arange(n, dtype=np.float32) / stride
+    i0 = t.astype(np.int64)
+    f = (t - i0)[:, None]
+    return ((1 - f) * zc[i0] + f * zc[i0 + 1]).astype(np.float32)
+
+
+def _llm_rope_kv(args):
+    """One kv-head of llm_rope and the q-heads of its group that are wanted."""
+    (seed, b, g_kv, hs, N, d, gamma, alpha, noise, rho, head_jitter, sink, sink_pairs, vmean,
+     v_noise, base) = args
+    f32 = np.float32
+    h2 = d // 2
+    low = np.r_[h2 - sink_pairs:h2, d - sink_pairs:d]       # lowest-frequency pairs
+    g = _rng([seed, b, 2000 + g_kv])
+    c = g.standard_normal(d, dtype=f32)
+    z = _ar1_coarse(g, N, d, rho)
+    wk = g.standard_normal((d, d), dtype=f32) / f32(math.sqrt(d))
+    kc = (c + f32(head_jitter) * g.standard_normal(d, dtype=f32)) + f32(alpha) * (z @ wk) \
+        + f32(noise) * g.standard_normal((N, d), dtype=f32)
+    kk = f32(gamma) * rope(kc, base)
+    # sink: q_t . k_0 / sqrt(d) ~ sink * gamma^2 |c|^2 / sqrt(d) for every t
+    s0 = np.zeros(d, f32)
+    s0[low] = c[low] * f32(d / (2 * sink_pairs) * sink)
+    kk[0] = f32(gamma) * s0
+    mu = g.standard_normal(d, dtype=f32)
+    wv = g.standard_normal((d, d), dtype=f32) / f32(math.sqrt(d))
+    vv = f32(vmean) * mu[None, :] + z @ wv + f32(v_noise) * g.standard_normal((N, d), dtype=f32)
+    qs = {}
+    for h in hs:
+        gh = _rng([seed, b, 3000 + h])
+        wq = wk + f32(head_jitter) * gh.standard_normal((d, d), dtype=f32) / f32(math.sqrt(d))
+        qc = (c + f32(head_jitter) * gh.standard_normal(d, dtype=f32)) + f32(alpha) * (z @ wq) \
+            + f32(noise) * gh.standard_normal((N, d), dtype=f32)
+        qs[h] = f32(gamma) * rope(qc, base)
+    return kk, vv, qs
+
+
 def llm_rope(seed, N, d=128, Hq=32, Hkv=8, B=1, gamma=0.9, alpha=0.05, noise=0.05, rho=0.998,
              head_jitter=0.3, sink=0.85, sink_pairs=8, vmean=1.0, v_noise=0.5, base=500000.0,
-             heads=None):
+             heads=None, workers=None):
     """C2 / C5.  Per kv-head g: content c ~ N(0, I_d), AR(1)
     latent z; K_s = gamma RoPE_s(c + e_k + alpha z_s W_k + noise);
     per q-head h of the group Q_t = gamma RoPE_t(c + e_h + alpha z_t W_q,h +
     noise) (e_k, e_h: head jitter); key 0 is a sink whose logit against every
     query is ~sink x the diagonal logit (its energy sits in the `sink_pairs`
     lowest RoPE frequencies, so it is position-independent); V = vmean mu +
-    z W_v + v_noise eps.  ``heads`` restricts generation to a list of global
-    q-heads (their kv-heads too); every head is seeded by its global index,
-    so a subset equals the same slice of the full tensor."""
+    z W_v + v_noise eps.  float32 arithmetic.  ``heads`` restricts generation
+    to a list of global q-heads (their kv-heads too); every head is seeded by
+    its global index, so a subset equals the same slice of the full tensor.
+    workers > 1 generates kv-heads in parallel processes (same result)."""
     group = Hq // Hkv
     hq_list = list(range(Hq)) if heads is None else list(heads)
     kv_list = sorted({h // group for h in hq_list})
     q = np.empty((B, len(hq_list), N, d), np.float32)
     k = np.empty((B, len(kv_list), N, d), np.float32)
     v = np.empty((B, len(kv_list), N, d), np.float32)
-    h2 = d // 2
-    low = np.r_[h2 - sink_pairs:h2, d - sink_pairs:d]       # lowest-frequency pairs
-    for b in range(B):
-        for a, g_kv in enumerate(kv_list):
-            g = _rng([seed, b, 2000 + g_kv])
-            c = g.standard_normal(d)
-            z = _ar1(g, N, d, rho)
-            wk = g.standard_normal((d, d)) / math.sqrt(d)
-            kc = c + head_jitter * g.standard_normal(d) + alpha * (z @ wk) \
-                + noise * g.standard_normal((N, d))
-            kk = gamma * rope(kc, base)
-            # sink: q_t . k_0 / sqrt(d) ~ sink * gamma^2 |c|^2 / sqrt(d) for every t
-            s0 = np.zeros(d)
-            s0[low] = c[low] * (d / (2 * sink_pairs)) * sink
-            kk[0] = gamma * s0
-            k[b, a] = kk
-            mu = g.standard_normal(d)
-            wv = g.standard_normal((d, d)) / math.sqrt(d)
-            v[b, a] = vmean * mu[None, :] + z @ wv + v_noise * g.standard_normal((N, d))
-            for h in range(g_kv * group, (g_kv + 1) * group):
-                if h not in hq_list:
-                    continue
-                gh = _rng([seed, b, 3000 + h])
-                wq = wk + head_jitter * gh.standard_normal((d, d)) / math.sqrt(d)
-                qc = c + head_jitter * gh.standard_normal(d) + alpha * (z @ wq) \
-                    + noise * gh.standard_normal((N, d))
-                q[b, hq_list.index(h)] = gamma * rope(qc, base)
+    jobs = [(seed, b, g_kv, [h for h in range(g_kv * group, (g_kv + 1) * group) if h in hq_list],
+             N, d, gamma, alpha, noise, rho, head_jitter, sink, sink_pairs, vmean, v_noise, base)
+            for b in range(B) for g_kv in kv_list]
+    if workers is None:
+        workers = min(len(jobs), 16) if N * len(jobs) >= (1 << 20) else 1
+    if workers > 1:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(workers) as pool:
+            outs = pool.map(_llm_rope_kv, jobs)
+    else:
+        outs = [_llm_rope_kv(j) for j in jobs]
+    for job, (kk, vv, qs) in zip(jobs, outs):
+        b, a = job[1], kv_list.index(job[2])
+        k[b, a] = kk
+        v[b, a] = vv
+        for h, qq in qs.items():
+            q[b, hq_list.index(h)] = qq
     return q, k, v
 
 
@@ -246,3 +296,20 @@ WORKLOADS = {
     "sweep_128k": dict(kind="llm_rope", N=131072, d=128, Hq=32, Hkv=32, causal=False),
 }
 HYPER = dict(tau=0.9, theta=0.5, lam=-5.0)
+
+# The §3.6 tuner's triple per workload at the paper's (l1, l2)
+# bounds, five calibration inputs, full size -- copied from
+# profiles/r02_f2_tuned.json (scripts/tune_workloads.py on a B200; the CPU test
+# tests/test_inputs_cpu.py checks the two agree).  bench.py's default triple.
+TUNED = {
+    "llama31_8b_32k": dict(tau=0.96, theta=0.4, **{"lambda": -10.0}, l1_bound=0.08),
+    "sweep_8k": dict(tau=0.9, theta=0.6, **{"lambda": -8.0}, l1_bound=0.08),
+    "sweep_16k": dict(tau=0.9, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
+    "sweep_32k": dict(tau=0.88, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
+    "sweep_64k": dict(tau=0.88, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
+    "sweep_128k": dict(tau=0.8, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
+    "cogvideox_2b": dict(tau=0.98, theta=0.6, **{"lambda": -4.0}, l1_bound=0.05),
+    "mochi": dict(tau=0.98, theta=0.2, **{"lambda": -4.0}, l1_bound=0.05),
+    "mochi_22k": dict(tau=0.98, theta=0.6, **{"lambda": -4.0}, l1_bound=0.05),
+    "flux": dict(tau=0.96, theta=0.6, **{"lambda": -4.0}, l1_bound=0.07),
+}
