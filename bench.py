@@ -311,6 +311,8 @@ def all_sum(vals, dev):
     """Sum host numbers over ranks (counters / L1 sums)."""
     import torch
     import torch.distributed as dist
+    if dist.is_initialized() and dist.get_backend() == "gloo":
+        dev = "cpu"
     t = torch.tensor([float(x) for x in vals], dtype=torch.float64, device=dev)
     if dist.is_initialized():
         dist.all_reduce(t)
@@ -453,10 +455,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SPARGE_BENCH_ONE_GPU=1 (plumbing checks on a 1-GPU box only: every rank
+    # on cuda:0, gloo instead of NCCL -- timings are then meaningless)
+    one_gpu = os.environ.get("SPARGE_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)        # before NCCL init: one GPU per rank
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = hyper(workload_cfg(args.workload), args.workload, args.triple)
     for key in ("tau", "theta", "lam"):
         if getattr(args, key) is not None:

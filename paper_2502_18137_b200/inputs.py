@@ -302,11 +302,11 @@ HYPER = dict(tau=0.9, theta=0.5, lam=-5.0)
 # profiles/r02_f2_tuned.json (scripts/tune_workloads.py on a B200; the CPU test
 # tests/test_inputs_cpu.py checks the two agree).  bench.py's default triple.
 TUNED = {
-    "llama31_8b_32k": dict(tau=0.96, theta=0.4, **{"lambda": -10.0}, l1_bound=0.08),
-    "sweep_8k": dict(tau=0.9, theta=0.6, **{"lambda": -8.0}, l1_bound=0.08),
+    "llama31_8b_32k": dict(tau=0.94, theta=0.4, **{"lambda": -10.0}, l1_bound=0.08),
+    "sweep_8k": dict(tau=0.92, theta=0.4, **{"lambda": -6.0}, l1_bound=0.08),
     "sweep_16k": dict(tau=0.9, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
     "sweep_32k": dict(tau=0.88, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
-    "sweep_64k": dict(tau=0.88, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
+    "sweep_64k": dict(tau=0.84, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
     "sweep_128k": dict(tau=0.8, theta=0.4, **{"lambda": -8.0}, l1_bound=0.08),
     "cogvideox_2b": dict(tau=0.98, theta=0.6, **{"lambda": -4.0}, l1_bound=0.05),
     "mochi": dict(tau=0.98, theta=0.2, **{"lambda": -4.0}, l1_bound=0.05),

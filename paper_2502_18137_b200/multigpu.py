@@ -41,11 +41,15 @@ def gather_heads(o_local, Hq, Hkv):
              for r in range(world)]
     mx = max(sizes)
     B, hr, N, d = o_local.shape
-    pad = o_local.new_zeros((B, mx, N, d))
-    pad[:, :hr] = o_local
+    dev = o_local.device
+    # gloo gathers host tensors (the CPU tests; NCCL gathers device memory)
+    host = dist.get_backend() == "gloo"
+    src = o_local.cpu() if host else o_local
+    pad = src.new_zeros((B, mx, N, d))
+    pad[:, :hr] = src
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad.contiguous())
-    return torch.cat([p[:, :s] for p, s in zip(parts, sizes)], dim=1)
+    return torch.cat([p[:, :s] for p, s in zip(parts, sizes)], dim=1).to(dev)
 
 
 def max_over_ranks(x, device=None):
@@ -53,6 +57,8 @@ def max_over_ranks(x, device=None):
     world, _ = world_rank()
     if world == 1:
         return x
+    if dist.get_backend() == "gloo":
+        device = "cpu"
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
