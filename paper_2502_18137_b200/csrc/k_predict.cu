@@ -20,7 +20,9 @@
 //               sort-free binned TopCdf selection (topcdf_binned: fixed-point
 //               integer bin masses, only the boundary bin sorted), forcing,
 //               causal AND + guard, ballot compaction into the LUT.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cfloat>
 
 #include "sparge_internal.h"
@@ -128,6 +130,15 @@ constexpr int kMaxRowWarps = 4;
 constexpr int kIdxBits = 16;
 constexpr uint64_t kIdxMask = (1ull << kIdxBits) - 1;
 constexpr size_t kRowSmemMax = 200 * 1024;
+// rows longer than this use k_topcdf_cta (env SPARGE_TOPCDF_CTA_MIN_TN
+// overrides for A/B runs; default measured on B200)
+int cta_row_min_tn() {
+  static const int v = [] {
+    const char* e = std::getenv("SPARGE_TOPCDF_CTA_MIN_TN");
+    return e ? std::atoi(e) : 512;
+  }();
+  return v;
+}
 constexpr int kNB = 256;
 __host__ __device__ inline int pow2ceil(int n) {
   int p = 32;
@@ -393,6 +404,276 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   if (lane == 0) cnt[row] = base;
 }
 
+// ---------------------------------------------------------------- TopCdf, CTA per row
+// The same selection as k_topcdf_rows with one CTA of kCtaWarps warps per
+// row, for long rows (T_n large): a row's keys take pow2ceil(T_n) * 8 bytes of
+// shared memory, so one warp per row left an SM with 8 warps at T_n = 2048
+// (12.5 % occupancy, ncu r02_pred128k); a CTA per row keeps ~40 warps busy.
+// Streaming phases split j across the warps; reductions go through shared
+// memory in a fixed order (deterministic); the boundary bin (usually small)
+// is compacted, sorted and scanned by warp 0.
+constexpr int kCtaWarps = 4;
+constexpr int kCtaThreads = kCtaWarps * 32;
+constexpr int kListCap = 1024;   // boundary entries gathered outside the key array
+
+__host__ __device__ inline size_t cta_row_smem_bytes(int T_n) {
+  return static_cast<size_t>(pow2ceil(T_n)) * 8 + kNB * 8 + kListCap * 8 + ((T_n + 15) / 16) * 16;
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+  v = warp_max(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double r = red[0];
+#pragma unroll
+  for (int w = 1; w < kCtaWarps; ++w) r = fmax(r, red[w]);
+  return r;
+}
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double r = red[0];
+#pragma unroll
+  for (int w = 1; w < kCtaWarps; ++w) r += red[w];       // fixed order
+  return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kCtaThreads)
+k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
+             const double* __restrict__ k_sim, int Hq, int Hkv, int N, int T_m, int T_n,
+             int bq, int bk, int causal, double tau, double theta,
+             uint8_t* __restrict__ mask, int32_t* __restrict__ lut, int32_t* __restrict__ cnt) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[kCtaWarps];
+  __shared__ unsigned long long red_u[kCtaWarps];
+  __shared__ int s_info[4];                 // bmin, m (boundary entries), list overflow
+  __shared__ unsigned long long s_astar;
+  __shared__ int s_wcount[kCtaWarps];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int row = blockIdx.x;               // (b*Hq + hq)*T_m + i
+  uint64_t* ukey = reinterpret_cast<uint64_t*>(smem);
+  double* key = reinterpret_cast<double*>(ukey);
+  const size_t nk = static_cast<size_t>(pow2ceil(T_n));
+  unsigned long long* bsum = reinterpret_cast<unsigned long long*>(smem + nk * 8);
+  uint64_t* list = reinterpret_cast<uint64_t*>(smem + nk * 8 + kNB * 8);
+  uint8_t* flag = smem + nk * 8 + kNB * 8 + kListCap * 8;
+
+  const int i = row % T_m, bhq = row / T_m;
+  const int hq = bhq % Hq, b = bhq / Hq;
+  const int64_t kbase = (static_cast<int64_t>(b) * Hkv + hq / (Hq / Hkv)) * T_n;
+  const int last_q = min((i + 1) * bq, N) - 1;
+  const int n_live = causal ? min(T_n, last_q / bk + 1) : T_n;
+  const double* srow = shat + static_cast<int64_t>(row) * T_n;
+
+  // ---- S^ row with the -inf columns (fixed K blocks, causally dead) ----
+  constexpr int kLoadBatch = 4;
+  double mx = -INFINITY;
+  for (int j0 = tid; j0 < T_n; j0 += kCtaThreads * kLoadBatch) {
+    double sv[kLoadBatch], kv[kLoadBatch];
+#pragma unroll
+    for (int u = 0; u < kLoadBatch; ++u) {
+      const int j = j0 + kCtaThreads * u;
+      sv[u] = (j < n_live) ? __ldg(srow + j) : -INFINITY;
+      kv[u] = (j < n_live) ? __ldg(k_sim + kbase + j) : 1.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kLoadBatch; ++u) {
+      const int j = j0 + kCtaThreads * u;
+      if (j < T_n) {
+        const double sj = (kv[u] < theta) ? -INFINITY : sv[u];
+        key[j] = sj;
+        mx = fmax(mx, sj);
+      }
+    }
+  }
+  for (int t = tid; t < kNB; t += kCtaThreads) bsum[t] = 0ull;
+  mx = block_max(mx, red);
+  const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
+
+  if (!flagged) {
+    double part = 0.0;
+    for (int j = tid; j < T_n; j += kCtaThreads) {
+      const double kv = key[j];
+      const double e = (kv == -INFINITY) ? 0.0 : exp(kv - mx);
+      key[j] = e;
+      part += e;
+    }
+    const double total = block_sum(part, red);
+    // keys (P^ bits, low kIdxBits replaced by kIdxMask - j) and the max key
+    uint64_t kmax = 0;
+    for (int j = tid; j < T_n; j += kCtaThreads) {
+      const uint64_t k = (static_cast<uint64_t>(__double_as_longlong(key[j] / total)) & ~kIdxMask) |
+                         static_cast<uint64_t>(kIdxMask - j);
+      ukey[j] = k;
+      kmax = max(kmax, k);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    __syncthreads();
+    if (lane == 0) red_u[wid] = kmax;
+    __syncthreads();
+    kmax = red_u[0];
+#pragma unroll
+    for (int w = 1; w < kCtaWarps; ++w) kmax = max(kmax, static_cast<uint64_t>(red_u[w]));
+    const int emax = static_cast<int>(kmax >> 52) & 0x7FF;
+    const int sc = min(52 - (emax - 1023), 63);     // as topcdf_binned
+    unsigned long long qpart = 0;
+    for (int j = tid; j < T_n; j += kCtaThreads) {
+      const uint64_t k = ukey[j];
+      const unsigned long long qj = __double2ull_rz(ldexp(__longlong_as_double(k & ~kIdxMask), sc));
+      atomicAdd(&bsum[bin_of(k, emax)], qj);
+      qpart += qj;
+    }
+    qpart = warp_sum_u64(qpart);
+    __syncthreads();                                 // bsum complete; red_u reuse
+    if (lane == 0) red_u[wid] = qpart;
+    __syncthreads();
+    unsigned long long qtotal = 0;
+#pragma unroll
+    for (int w = 0; w < kCtaWarps; ++w) qtotal += red_u[w];
+    const double thr = (tau >= 1.0) ? INFINITY : tau * static_cast<double>(qtotal);
+    // boundary bin by warp 0 (lane-parallel prefix over the NB bins)
+    if (wid == 0) {
+      unsigned long long lsum = 0;
+#pragma unroll
+      for (int u = 0; u < kNB / 32; ++u) lsum += bsum[lane * (kNB / 32) + u];
+      unsigned long long incl = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      unsigned long long above = incl - lsum;
+      int bstar = kNB;
+      unsigned long long a_star = 0;
+#pragma unroll
+      for (int u = 0; u < kNB / 32; ++u) {
+        const int bb = lane * (kNB / 32) + u;
+        const unsigned long long nxt = above + bsum[bb];
+        if (bstar == kNB && static_cast<double>(nxt) > thr) { bstar = bb; a_star = above; }
+        above = nxt;
+      }
+      int bmin = bstar;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+      const unsigned int owner = __ballot_sync(0xffffffffu, bstar == bmin && bmin < kNB);
+      if (bmin < kNB) a_star = __shfl_sync(0xffffffffu, a_star, __ffs(owner) - 1);
+      if (lane == 0) {
+        s_info[0] = bmin;
+        s_info[1] = 0;
+        s_astar = a_star;
+      }
+    }
+    __syncthreads();
+    const int bmin = s_info[0];
+    // flags outside the boundary bin; the boundary entries gathered into
+    // `list` (order irrelevant: sorted below) while they fit kListCap
+    for (int j0 = wid * 32; j0 < T_n; j0 += kCtaThreads) {
+      const int j = j0 + lane;
+      const uint64_t k = (j < T_n) ? ukey[j] : 0ull;
+      const int bb = (j < T_n) ? bin_of(k, emax) : kNB;
+      const bool inb = (j < T_n) && (bb == bmin);
+      if (j < T_n) flag[j] = (bb < bmin) ? 1 : 0;
+      const unsigned int bal = __ballot_sync(0xffffffffu, inb);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&s_info[1], __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int pos = base + __popc(bal & ((1u << lane) - 1u));
+      if (inb && pos < kListCap) list[pos] = k;
+    }
+    __syncthreads();
+    const int m = s_info[1];
+    if (wid == 0 && bmin < kNB) {
+      uint64_t* lst = list;
+      if (m > kListCap) {
+        // rare (a huge boundary bin, e.g. near-uniform P^): warp 0 alone
+        // compacts the bin in place in the key array, as topcdf_binned does
+        lst = ukey;
+        int mm = 0;
+        for (int j0 = 0; j0 < T_n; j0 += 32) {
+          const int j = j0 + lane;
+          const uint64_t k = (j < T_n) ? ukey[j] : 0ull;
+          const bool inb = (j < T_n) && (bin_of(k, emax) == bmin);
+          const unsigned int bal = __ballot_sync(0xffffffffu, inb);
+          __syncwarp();
+          if (inb) lst[mm + __popc(bal & ((1u << lane) - 1u))] = k;
+          mm += __popc(bal);
+          __syncwarp();
+        }
+      }
+      int n2 = 2;
+      while (n2 < m) n2 <<= 1;
+      for (int t = m + lane; t < n2; t += 32) lst[t] = 0ull;
+      __syncwarp();
+      sort_desc_n(lst, n2, lane);
+      unsigned long long carry = s_astar;
+      for (int t0 = 0; t0 < m; t0 += 32) {
+        const int t = t0 + lane;
+        const uint64_t k = (t < m) ? lst[t] : 0ull;
+        unsigned long long qv =
+            (t < m) ? __double2ull_rz(ldexp(__longlong_as_double(k & ~kIdxMask), sc)) : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long y = __shfl_up_sync(0xffffffffu, qv, o);
+          if (lane >= o) qv += y;
+        }
+        const unsigned long long c = carry + qv;
+        if (t < m) flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (static_cast<double>(c) <= thr) ? 1 : 0;
+        carry = __shfl_sync(0xffffffffu, c, 31);
+      }
+    }
+    if (tid == 0) flag[kIdxMask - static_cast<int>(kmax & kIdxMask)] = 1;   // guard
+  }
+  __syncthreads();
+
+  // ---- forcing (Eq. 5), flagged rows, causal live AND + diagonal guard;
+  // LUT in ascending j: warp w owns the contiguous chunk [w*ch, (w+1)*ch) ----
+  const bool row_fix = q_sim[row] < theta;
+  const int guard = (i * bq) / bk;
+  uint8_t* mrow = mask ? mask + static_cast<int64_t>(row) * T_n : nullptr;
+  int32_t* lrow = lut + static_cast<int64_t>(row) * T_n;
+  const int ch = ((T_n + kCtaWarps - 1) / kCtaWarps + 31) / 32 * 32;
+  const int c0 = wid * ch, c1 = min(T_n, c0 + ch);
+  auto kept = [&](int j) {
+    bool f = flagged ? true : (flag[j] != 0);
+    if (row_fix || (j < n_live && k_sim[kbase + j] < theta)) f = true;
+    if (causal) {
+      if (j >= n_live) f = false;
+      if (j == guard) f = true;
+    }
+    return f;
+  };
+  int wc = 0;
+  for (int j0 = c0; j0 < c1; j0 += 32) {
+    const int j = j0 + lane;
+    const bool f = (j < c1) && kept(j);
+    if (j < c1 && mrow) mrow[j] = f ? 1 : 0;
+    wc += __popc(__ballot_sync(0xffffffffu, f));
+  }
+  if (lane == 0) s_wcount[wid] = wc;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < wid; ++w) base += s_wcount[w];
+  for (int j0 = c0; j0 < c1; j0 += 32) {
+    const int j = j0 + lane;
+    const bool f = (j < c1) && kept(j);
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (f) lrow[base + __popc(bal & ((1u << lane) - 1u))] = j;
+    base += __popc(bal);
+  }
+  if (tid == 0) {
+    int total = 0;
+    for (int w = 0; w < kCtaWarps; ++w) total += s_wcount[w];
+    cnt[row] = total;
+  }
+}
+
 template <int D>
 cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double* q_sim,
                      const double* k_pooled, const double* k_sim, float tau, float theta,
@@ -407,12 +688,24 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
   dim3 g1((T_n + kTile - 1) / kTile, (T_m + kTile - 1) / kTile, s.B * s.Hq);
   k_shat_dmma<D><<<g1, kGemmThreads, smem_g, stream>>>(q_pooled, k_pooled, s.Hq, s.Hkv, T_m, T_n,
                                                         s.N, s.bq, s.bk, s.causal, shat);
+  const int rows = s.B * s.Hq * T_m;
+  // long rows: one CTA of kCtaWarps warps per row (occupancy); short rows:
+  // one warp per row, up to kMaxRowWarps rows per CTA
+  if (T_n > cta_row_min_tn()) {
+    const size_t smem_c = cta_row_smem_bytes(T_n);
+    e = cudaFuncSetAttribute(k_topcdf_cta<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem_c));
+    if (e != cudaSuccess) return e;
+    k_topcdf_cta<D><<<rows, kCtaThreads, smem_c, stream>>>(
+        shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, s.bq, s.bk, s.causal,
+        static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
+    return cudaGetLastError();
+  }
   // rows per CTA: up to kMaxRowWarps, as many as fit the shared memory
   const size_t per_warp = row_smem_bytes(T_n);
   const int warps = static_cast<int>(std::min<size_t>(kMaxRowWarps, kRowSmemMax / per_warp));
   if (warps < 1) return cudaErrorInvalidValue;
   const size_t smem_r = per_warp * warps;
-  const int rows = s.B * s.Hq * T_m;
   e = cudaFuncSetAttribute(k_topcdf_rows<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem_r));
   if (e != cudaSuccess) return e;
