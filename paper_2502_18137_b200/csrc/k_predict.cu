@@ -32,15 +32,18 @@ namespace sparge {
 namespace {
 
 // ---------------------------------------------------------------- S^ GEMM
+// v2 (round 2): 64 query blocks x 64 key blocks per CTA, the d axis staged in
+// chunks of kKC doubles through a double-buffered cp.async ring (loads of
+// chunk c+1 overlap the DMMAs of chunk c; 37 KB per stage, so several CTAs
+// share an SM -- v1 staged all of d at once, 135 KB, one CTA per SM, and the
+// SM idled during every load: 25 % occupancy, ncu r02_pred128k); 8 warps,
+// each a 16-row x 32-key register tile (2 x 4 DMMA fragments per k-step:
+// 6 fragment loads per 8 DMMAs).
 constexpr int kTile = 64;          // query blocks x key blocks per CTA
-#ifdef SPARGE_SHAT_8WARPS
-constexpr int kColSplit = 1;       // 8 warps, one 8-row strip x 64 keys each
-#elif defined(SPARGE_SHAT_COLSPLIT)
-constexpr int kColSplit = SPARGE_SHAT_COLSPLIT;
-#else
-constexpr int kColSplit = 2;       // 16 warps, one 8-row strip x 32 keys each
-#endif
-constexpr int kGemmThreads = 256 * kColSplit;
+constexpr int kKC = 32;            // d chunk (doubles) per stage
+constexpr int kKR = kKC + 4;       // padded chunk row: kKR % 16 == 4 (conflict-free fragments)
+constexpr int kGemmThreads = 256;
+constexpr size_t kGemmSmem = sizeof(double) * 2 /*stages*/ * 2 /*Q, K*/ * kTile * kKR;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
@@ -57,10 +60,9 @@ __global__ void __launch_bounds__(kGemmThreads)
 k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_pooled,
             int Hq, int Hkv, int T_m, int T_n, int N, int bq, int bk, int causal,
             double* __restrict__ shat) {
-  constexpr int KR = D + 4;         // padded row (doubles): KR % 16 == 4
+  constexpr int NCH = D / kKC;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* sq = reinterpret_cast<double*>(smem);          // [kTile][KR]
-  double* sk = sq + kTile * KR;                          // [kTile][KR]
+  double* stage = reinterpret_cast<double*>(smem);       // [2][2][kTile][kKR]
   const int j0 = blockIdx.x * kTile, i0 = blockIdx.y * kTile, bhq = blockIdx.z;
   // causal: a tile whose every key block is dead for every query block of
   // the tile (R8-i) is never read by k_topcdf_rows -- skip it
@@ -71,51 +73,75 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
   const int64_t kbase = (static_cast<int64_t>(b) * Hkv + hkv) * T_n;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
-  // stage 64 pooled-Q rows and 64 pooled-K rows (zero beyond T_m / T_n)
-  constexpr int CH = D / 2;         // 16-B chunks per row
-  for (int e = tid; e < 2 * kTile * CH; e += kGemmThreads) {
-    const int which = e / (kTile * CH);
-    const int rr = (e / CH) % kTile, cc = e % CH;
-    double* dst = (which ? sk : sq) + rr * KR + 2 * cc;
-    const bool ok = which ? (j0 + rr < T_n) : (i0 + rr < T_m);
-    if (ok) {
-      const double* src = which ? k_pooled + (kbase + j0 + rr) * D + 2 * cc
-                                : q_pooled + (qbase + i0 + rr) * D + 2 * cc;
-      cp_async16(dst, src);
-    } else {
-      dst[0] = 0.0;
-      dst[1] = 0.0;
+  // chunk c of 64 pooled-Q rows and 64 pooled-K rows (zero beyond T_m / T_n)
+  auto issue = [&](int c, int buf) {
+    double* sq = stage + (buf * 2 + 0) * kTile * kKR;
+    double* sk = stage + (buf * 2 + 1) * kTile * kKR;
+    constexpr int CH = kKC / 2;      // 16-B pieces per chunk row
+    for (int e = tid; e < 2 * kTile * CH; e += kGemmThreads) {
+      const int which = e / (kTile * CH);
+      const int rr = (e / CH) % kTile, cc = e % CH;
+      double* dst = (which ? sk : sq) + rr * kKR + 2 * cc;
+      const bool ok = which ? (j0 + rr < T_n) : (i0 + rr < T_m);
+      if (ok) {
+        const double* src = which ? k_pooled + (kbase + j0 + rr) * D + c * kKC + 2 * cc
+                                  : q_pooled + (qbase + i0 + rr) * D + c * kKC + 2 * cc;
+        cp_async16(dst, src);
+      } else {
+        dst[0] = 0.0;
+        dst[1] = 0.0;
+      }
     }
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
 
-  // warp wid: rows 8*(wid%8)..+7 against keys [cq*NKT*8, (cq+1)*NKT*8),
-  // cq = wid/8 (NKT DMMA tiles); fragments (m8n8k4, f64): A row = lane/4,
-  // k = lane%4; B k = lane%4, n = lane/4; C row = lane/4, cols 2*(lane%4) + {0,1}
-  constexpr int NKT = 8 / kColSplit;
-  const int strip = wid & 7, cq = wid >> 3;
+  // warp w: rows 16*(w%4)..+15 (two 8-row fragments) x keys 32*(w/4)..+31
+  // (four 8-key fragments); fragments (m8n8k4, f64): A row = lane/4,
+  // k = lane%4; B k = lane%4, n = lane/4; C row = lane/4, cols 2*(lane%4)+{0,1}
+  const int rs = wid & 3, kh = wid >> 2;
   const int g = lane >> 2, t4 = lane & 3;
-  double acc[NKT][2];
+  double acc[2][4][2];
 #pragma unroll
-  for (int kt = 0; kt < NKT; ++kt) acc[kt][0] = acc[kt][1] = 0.0;
-  const double* arow = sq + (8 * strip + g) * KR + t4;
-  const double* brow = sk + (cq * NKT * 8 + g) * KR + t4;
-#pragma unroll 4
-  for (int ks = 0; ks < D / 4; ++ks) {
-    const double a = arow[4 * ks];
+  for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int kt = 0; kt < NKT; ++kt) dmma_884(acc[kt][0], acc[kt][1], a, brow[8 * kt * KR + 4 * ks]);
+    for (int kt = 0; kt < 4; ++kt) acc[r][kt][0] = acc[r][kt][1] = 0.0;
+
+  issue(0, 0);
+  for (int c = 0; c < NCH; ++c) {
+    if (c + 1 < NCH) {
+      issue(c + 1, (c + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* sq = stage + ((c & 1) * 2 + 0) * kTile * kKR;
+    const double* sk = stage + ((c & 1) * 2 + 1) * kTile * kKR;
+    const double* a0 = sq + (16 * rs + g) * kKR + t4;
+    const double* b0 = sk + (32 * kh + g) * kKR + t4;
+#pragma unroll
+    for (int ks = 0; ks < kKC / 4; ++ks) {
+      const double a_lo = a0[4 * ks], a_hi = a0[8 * kKR + 4 * ks];
+#pragma unroll
+      for (int kt = 0; kt < 4; ++kt) {
+        const double bv = b0[8 * kt * kKR + 4 * ks];
+        dmma_884(acc[0][kt][0], acc[0][kt][1], a_lo, bv);
+        dmma_884(acc[1][kt][0], acc[1][kt][1], a_hi, bv);
+      }
+    }
+    __syncthreads();          // the buffer is refilled two chunks later
   }
   const double inv_sqrt_d = 1.0 / sqrt(static_cast<double>(D));
-  const int row = i0 + 8 * strip + g;
-  if (row < T_m) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int row = i0 + 16 * rs + 8 * r + g;
+    if (row >= T_m) continue;
     double* out = shat + (qbase + row) * T_n;
 #pragma unroll
-    for (int kt = 0; kt < NKT; ++kt) {
-      const int key = j0 + cq * NKT * 8 + 8 * kt + 2 * t4;
-      if (key < T_n) out[key] = acc[kt][0] * inv_sqrt_d;
-      if (key + 1 < T_n) out[key + 1] = acc[kt][1] * inv_sqrt_d;
+    for (int kt = 0; kt < 4; ++kt) {
+      const int key = j0 + 32 * kh + 8 * kt + 2 * t4;
+      if (key < T_n) out[key] = acc[r][kt][0] * inv_sqrt_d;
+      if (key + 1 < T_n) out[key + 1] = acc[r][kt][1] * inv_sqrt_d;
     }
   }
 }
@@ -135,7 +161,7 @@ constexpr size_t kRowSmemMax = 200 * 1024;
 int cta_row_min_tn() {
   static const int v = [] {
     const char* e = std::getenv("SPARGE_TOPCDF_CTA_MIN_TN");
-    return e ? std::atoi(e) : 512;
+    return e ? std::atoi(e) : 1024;
   }();
   return v;
 }
@@ -152,11 +178,6 @@ __host__ __device__ inline size_t row_smem_bytes(int T_n) {
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 // Warp-synchronous bitonic sort, descending, of n (a power of two) 64-bit
@@ -187,9 +208,9 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // TopCdf selection without a full sort (v4).  Keys as in the sort path
 // (truncated P^ bits | kIdxMask - j).  The selected set is a prefix of the
 // descending order, so only the entries of the BOUNDARY bin need ordering:
-//   * P^ is put in fixed point, q_j = floor(p_j * 2^s) with p_max * 2^s in
-//     [2^52, 2^53) or s = 63 (sum <= 2^63 (1 + eps) < 2^64 as P^ sums to
-//     1): integer sums are exact and order-free, so
+//   * P^ (here e = exp(S^ - max), the unnormalised P^) is put in fixed
+//     point, q_j = floor(e_j * 2^s) (fixed_point_scale: the sum < 2^64):
+//     integer sums are exact and order-free, so
 //     the result is deterministic and equals the sequential fp64 cumsum up
 //     to ~2^-52 relative (inside the 1e-6 near-threshold band);
 //   * bins by (binade below the max, top 3 mantissa bits): NB = 256 bins in
@@ -207,6 +228,16 @@ __device__ __forceinline__ int bin_of(uint64_t key, int emax) {
   if (db >= kNB / 8) return kNB - 1;
   return db * 8 + (7 - static_cast<int>((key >> 49) & 7u));
 }
+// q_j = floor(e_j 2^sc): the largest entry (e_max = 1, emax its exponent)
+// lands in [2^52, 2^53) unless T_n * 2^(52 + 1) could overflow the 64-bit sum,
+// then sc drops to 63 - ceil(log2 T_n) (T_n <= 2^14: sc >= 49; entries below
+// 2^-sc of the max become 0 -- a cumulative error <= T_n 2^-sc, far inside
+// the 1e-6 band)
+__device__ __forceinline__ int fixed_point_scale(int emax, int T_n) {
+  int lg = 0;
+  while ((1 << lg) < T_n) ++lg;
+  return min(52 - (emax - 1023), 63 - lg);
+}
 __device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t* flag, int T_n,
                               double tau, int lane) {
   auto kix = [](int j) { return j; };
@@ -217,9 +248,7 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t*
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
   const int emax = static_cast<int>(kmax >> 52) & 0x7FF;
-  // scale so that max q_j is in [2^52, 2^53) -- capped at 2^63 so the sum
-  // (P^ sums to 1) stays below 2^64 when T_n > 2^11 (p_max may be < 2^-11)
-  const int sc = min(52 - (emax - 1023), 63);
+  const int sc = fixed_point_scale(emax, T_n);
   for (int b = lane; b < kNB; b += 32) bsum[b] = 0ull;
   __syncwarp();
   unsigned long long part = 0;
@@ -359,22 +388,20 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
 
   if (!flagged) {
-    double part = 0.0;
+    // One 64-bit sort key per entry: the bits of e_j = exp(S^_j - max) (>= 0,
+    // so integer order = value order) with the low kIdxBits mantissa bits
+    // replaced by kIdxMask - j.  TopCdf's rule c_k <= tau c_last is
+    // homogeneous, so selecting on e is selecting on P^ = e / sum(e) (R4):
+    // the normalisation (a division per entry) is skipped.  Ordering the keys
+    // descending orders (P^ desc, j asc) up to a 2^-36 relative truncation --
+    // far inside the 1e-6 near-threshold band; the cumulative sums use the
+    // truncated values.
     for (int j = lane; j < T_n; j += 32) {
       const double kv = key[j];
       const double e = (kv == -INFINITY) ? 0.0 : exp(kv - mx);
-      key[j] = e;
-      part += e;
-    }
-    const double total = warp_sum(part);
-    // One 64-bit sort key per entry: the bits of P^ (>= 0, so integer order =
-    // value order) with the low kIdxBits mantissa bits replaced by kIdxMask - j.
-    // Ordering the keys descending orders (P^ desc, j asc) up to a 2^-36
-    // relative truncation of P^ -- far inside the 1e-6 near-threshold band of
-    // the parity criterion; the cumulative sums use the truncated values.
-    for (int j = lane; j < T_n; j += 32)
-      ukey[j] = (static_cast<uint64_t>(__double_as_longlong(key[j] / total)) & ~kIdxMask) |
+      ukey[j] = (static_cast<uint64_t>(__double_as_longlong(e)) & ~kIdxMask) |
                 static_cast<uint64_t>(kIdxMask - j);
+    }
     __syncwarp();
     topcdf_binned(ukey, bsum, flag, T_n, tau, lane);
   }
@@ -431,18 +458,6 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   for (int w = 1; w < kCtaWarps; ++w) r = fmax(r, red[w]);
   return r;
 }
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  double r = red[0];
-#pragma unroll
-  for (int w = 1; w < kCtaWarps; ++w) r += red[w];       // fixed order
-  return r;
-}
-
 template <int D>
 __global__ void __launch_bounds__(kCtaThreads)
 k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
@@ -497,18 +512,13 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
 
   if (!flagged) {
-    double part = 0.0;
+    // keys (bits of e = exp(S^ - max), low kIdxBits replaced by kIdxMask - j;
+    // unnormalised as in k_topcdf_rows) and the max key
+    uint64_t kmax = 0;
     for (int j = tid; j < T_n; j += kCtaThreads) {
       const double kv = key[j];
       const double e = (kv == -INFINITY) ? 0.0 : exp(kv - mx);
-      key[j] = e;
-      part += e;
-    }
-    const double total = block_sum(part, red);
-    // keys (P^ bits, low kIdxBits replaced by kIdxMask - j) and the max key
-    uint64_t kmax = 0;
-    for (int j = tid; j < T_n; j += kCtaThreads) {
-      const uint64_t k = (static_cast<uint64_t>(__double_as_longlong(key[j] / total)) & ~kIdxMask) |
+      const uint64_t k = (static_cast<uint64_t>(__double_as_longlong(e)) & ~kIdxMask) |
                          static_cast<uint64_t>(kIdxMask - j);
       ukey[j] = k;
       kmax = max(kmax, k);
@@ -522,7 +532,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
 #pragma unroll
     for (int w = 1; w < kCtaWarps; ++w) kmax = max(kmax, static_cast<uint64_t>(red_u[w]));
     const int emax = static_cast<int>(kmax >> 52) & 0x7FF;
-    const int sc = min(52 - (emax - 1023), 63);     // as topcdf_binned
+    const int sc = fixed_point_scale(emax, T_n);
     unsigned long long qpart = 0;
     for (int j = tid; j < T_n; j += kCtaThreads) {
       const uint64_t k = ukey[j];
@@ -681,7 +691,7 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
                      cudaStream_t stream) {
   const int T_m = (s.N + s.bq - 1) / s.bq;
   const int T_n = (s.N + s.bk - 1) / s.bk;
-  const size_t smem_g = sizeof(double) * 2 * kTile * (D + 4);
+  const size_t smem_g = kGemmSmem;
   cudaError_t e = cudaFuncSetAttribute(k_shat_dmma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem_g));
   if (e != cudaSuccess) return e;
