@@ -146,6 +146,35 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
   }
 }
 
+// e^x for x <= 0 in fp64 without the library's special-case paths: 2^t,
+// t = x log2(e), split t = n + f (n = rint t by the 1.5 * 2^52 trick,
+// |f| <= 1/2), 2^f by its degree-12 Taylor polynomial in f (relative error
+// < 5e-16 on [-1/2, 1/2]), 2^n added into the exponent; e^x < 2^-1000 -> 0
+// (such an entry carries no P^ mass at fp64 resolution).  Relative error
+// ~|t| 2^-53 from rounding t: < 1e-13 for |t| < 1000, far below the 1e-6
+// near-threshold band (R4, R15).
+__device__ __forceinline__ double exp_nonpos(double x) {
+  const double t = x * 1.4426950408889634;
+  if (!(t > -1000.0)) return 0.0;
+  const double r = t + 6755399441055744.0;            // 1.5 * 2^52: rounds t to an integer
+  const int n = static_cast<int>(__double2loint(r));  // low word = n (two's complement)
+  const double f = t - (r - 6755399441055744.0);
+  double p = 2.5678435993488196e-11;
+  p = fma(p, f, 4.44553827187081e-10);
+  p = fma(p, f, 7.054911620801121e-09);
+  p = fma(p, f, 1.0178086009239696e-07);
+  p = fma(p, f, 1.3215486790144305e-06);
+  p = fma(p, f, 1.5252733804059838e-05);
+  p = fma(p, f, 0.00015403530393381606);
+  p = fma(p, f, 0.0013333558146428441);
+  p = fma(p, f, 0.009618129107628477);
+  p = fma(p, f, 0.055504108664821576);
+  p = fma(p, f, 0.2402265069591007);
+  p = fma(p, f, 0.6931471805599453);
+  p = fma(p, f, 1.0);
+  return __hiloint2double(__double2hiint(p) + (n << 20), __double2loint(p));
+}
+
 // ---------------------------------------------------------------- TopCdf rows
 // k_topcdf_rows: up to kMaxRowWarps rows (one warp each) per CTA, each warp
 // holding its row in shared memory: pow2ceil(T_n) 64-bit keys (the boundary
@@ -398,7 +427,7 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
     // truncated values.
     for (int j = lane; j < T_n; j += 32) {
       const double kv = key[j];
-      const double e = (kv == -INFINITY) ? 0.0 : exp(kv - mx);
+      const double e = (kv == -INFINITY) ? 0.0 : exp_nonpos(kv - mx);
       ukey[j] = (static_cast<uint64_t>(__double_as_longlong(e)) & ~kIdxMask) |
                 static_cast<uint64_t>(kIdxMask - j);
     }
@@ -517,7 +546,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
     uint64_t kmax = 0;
     for (int j = tid; j < T_n; j += kCtaThreads) {
       const double kv = key[j];
-      const double e = (kv == -INFINITY) ? 0.0 : exp(kv - mx);
+      const double e = (kv == -INFINITY) ? 0.0 : exp_nonpos(kv - mx);
       const uint64_t k = (static_cast<uint64_t>(__double_as_longlong(e)) & ~kIdxMask) |
                          static_cast<uint64_t>(kIdxMask - j);
       ukey[j] = k;
