@@ -280,15 +280,22 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t*
   const int sc = fixed_point_scale(emax, T_n);
   for (int b = lane; b < kNB; b += 32) bsum[b] = 0ull;
   __syncwarp();
-  unsigned long long part = 0;
+  // the catch-all bin (>= 32 binades below the max: most entries of a
+  // peaked row) is summed in registers -- 32-way atomic conflicts otherwise
+  const double scale = ldexp(1.0, sc);
+  unsigned long long part = 0, q_last = 0;
   for (int j = lane; j < T_n; j += 32) {
     const uint64_t k = ukey[kix(j)];
-    const unsigned long long qj = __double2ull_rz(ldexp(__longlong_as_double(k & ~kIdxMask), sc));
+    const unsigned long long qj = __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale);
     const int b = bin_of(k, emax);
-    atomicAdd(&bsum[b], qj);
+    if (b == kNB - 1) q_last += qj;
+    else if (qj) atomicAdd(&bsum[b], qj);
     part += qj;
   }
   const unsigned long long total = warp_sum_u64(part);
+  q_last = warp_sum_u64(q_last);
+  __syncwarp();
+  if (lane == 0) bsum[kNB - 1] += q_last;
   __syncwarp();
   const double thr = (tau >= 1.0) ? INFINITY : tau * static_cast<double>(total);
   // boundary bin: lane-parallel prefix over the NB bins (8 per lane, in order)
@@ -345,7 +352,7 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t*
       const int t = t0 + lane;
       const uint64_t k = (t < m) ? list[t] : 0ull;
       unsigned long long qv =
-          (t < m) ? __double2ull_rz(ldexp(__longlong_as_double(k & ~kIdxMask), sc)) : 0ull;
+          (t < m) ? __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale) : 0ull;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long y = __shfl_up_sync(0xffffffffu, qv, o);
@@ -562,14 +569,19 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
     for (int w = 1; w < kCtaWarps; ++w) kmax = max(kmax, static_cast<uint64_t>(red_u[w]));
     const int emax = static_cast<int>(kmax >> 52) & 0x7FF;
     const int sc = fixed_point_scale(emax, T_n);
-    unsigned long long qpart = 0;
+    const double scale = ldexp(1.0, sc);
+    unsigned long long qpart = 0, q_last = 0;
     for (int j = tid; j < T_n; j += kCtaThreads) {
       const uint64_t k = ukey[j];
-      const unsigned long long qj = __double2ull_rz(ldexp(__longlong_as_double(k & ~kIdxMask), sc));
-      atomicAdd(&bsum[bin_of(k, emax)], qj);
+      const unsigned long long qj = __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale);
+      const int bb = bin_of(k, emax);
+      if (bb == kNB - 1) q_last += qj;              // catch-all bin in registers
+      else if (qj) atomicAdd(&bsum[bb], qj);
       qpart += qj;
     }
     qpart = warp_sum_u64(qpart);
+    q_last = warp_sum_u64(q_last);
+    if (lane == 0 && q_last) atomicAdd(&bsum[kNB - 1], q_last);
     __syncthreads();                                 // bsum complete; red_u reuse
     if (lane == 0) red_u[wid] = qpart;
     __syncthreads();
@@ -656,7 +668,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
         const int t = t0 + lane;
         const uint64_t k = (t < m) ? lst[t] : 0ull;
         unsigned long long qv =
-            (t < m) ? __double2ull_rz(ldexp(__longlong_as_double(k & ~kIdxMask), sc)) : 0ull;
+            (t < m) ? __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale) : 0ull;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const unsigned long long y = __shfl_up_sync(0xffffffffu, qv, o);
