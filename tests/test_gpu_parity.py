@@ -73,6 +73,37 @@ def test_quantize_literal_sim_and_perm(lib):
         np.testing.assert_allclose(si[0, h], O.block_sims(xp, 64, "literal"), rtol=1e-12)
 
 
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("is_key", [0, 1])
+@pytest.mark.parametrize("layout", ["contiguous", "strided", "perm"])
+def test_quantize_many_jobs(lib, d, is_key, layout):
+    """Thousands of slab jobs (every CTA of the persistent grid wraps its
+    slab ring several times), a ragged tail, and the three producer paths:
+    one bulk copy per contiguous slab, one per row for a strided [B,N,H,d]
+    view, one per gathered row through perm.  Checked on two heads."""
+    N, H = 32768 + 77, 8
+    xn = inputs.gaussian(11 + d + is_key, 1, H, N, d, scale=1.5)
+    if layout == "strided":
+        base = _dev(np.ascontiguousarray(xn.transpose(0, 2, 1, 3)))   # [B, N, H, d]
+        x = base.transpose(1, 2)                                        # view [B, H, N, d]
+        assert not x.is_contiguous()
+    else:
+        x = _dev(xn)
+    perm = None
+    if layout == "perm":
+        perm = np.random.default_rng(d + is_key).permutation(N).astype(np.int32)
+    xq, dl, po, si = _quant_case(lib, x, is_key, None if perm is None else torch.from_numpy(perm).cuda())
+    xs = bf16_np(x.contiguous())[0]
+    bs = 64 if is_key else 128
+    for h in (0, H - 1):
+        xh = xs[h] if perm is None else xs[h][perm]
+        q_ref, d_ref = O.quantize_blocks(xh, bs)
+        assert np.array_equal(xq[0, h], q_ref)
+        assert np.array_equal(dl[0, h], d_ref)
+        np.testing.assert_allclose(po[0, h], O.block_mean(xh, bs), rtol=0, atol=1e-13)
+        np.testing.assert_allclose(si[0, h], O.block_sims(xh, bs), rtol=1e-12, atol=1e-13)
+
+
 def _check_masks(gpu_mask, ref, label):
     mism = (gpu_mask != ref["M"])
     bad = mism & ~ref["near"]
