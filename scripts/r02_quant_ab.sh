@@ -11,5 +11,5 @@ for w in llama31_8b_32k cogvideox_2b mochi sweep_128k; do
 done; done
 cat $O/qab.txt
 ncu --set full --clock-control none --import-source on -k regex:k_quant_pool_sim -c 2 \
-  -o $O/qv13 -f python bench.py --profile --steps 1 --warmup 0 --no-sweep --no-cpu-baseline --no-f1 --no-e2e --no-dense > /dev/null 2>&1
-ncu -i $O/qv13.ncu-rep --page details --csv > $O/qv13_details.csv; ncu -i $O/qv13.ncu-rep --page raw --csv > $O/qv13_raw.csv; ncu -i $O/qv13.ncu-rep --page source --csv --print-source sass > $O/qv13_sass.csv 2>&1; ls -la $O/qv13*
+  -o $O/qv14 -f python bench.py --profile --steps 1 --warmup 0 --no-sweep --no-cpu-baseline --no-f1 --no-e2e --no-dense > /dev/null 2>&1
+ncu -i $O/qv14.ncu-rep --page details --csv > $O/qv14_details.csv; ncu -i $O/qv14.ncu-rep --page raw --csv > $O/qv14_raw.csv; ncu -i $O/qv14.ncu-rep --page source --csv --print-source sass > $O/qv14_sass.csv 2>&1; ls -la $O/qv14*
