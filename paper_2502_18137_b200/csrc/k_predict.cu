@@ -194,14 +194,37 @@ int cta_row_min_tn() {
   }();
   return v;
 }
+// first-level bins: 32 binades below the row max x SUB mantissa sub-bins
+// (the last bin is the catch-all for entries >= 31 binades down), 256 bins
+// (SUB 8); 1024 bins (SUB 32) measured slower in the CTA kernel (the bin
+// clearing and scan outweigh the smaller boundary sort)
 constexpr int kNB = 256;
+constexpr int kNBCta = 256;
 __host__ __device__ inline int pow2ceil(int n) {
   int p = 32;
   while (p < n) p <<= 1;
   return p;
 }
+// bin masses: three 32-bit partial sums per bin (bits 0-16, 17-33, 34-) of
+// the fixed-point masses, so each entry is three native shared-memory atomic
+// adds (a 64-bit shared atomicAdd is a CAS loop on sm_100: ATOMS.CAST.SPIN.64,
+// 20 % of the r02 TopCdf instructions); q < 2^51 per entry and T_n <= 2^14
+// keep every partial sum below 2^32
+__host__ __device__ inline size_t bins_bytes(int nb) { return static_cast<size_t>(nb) * 12; }
+__device__ __forceinline__ void bin_add(uint32_t* c, int nb, int b, unsigned long long q) {
+  atomicAdd(c + b, static_cast<uint32_t>(q & 0x1FFFFu));
+  atomicAdd(c + nb + b, static_cast<uint32_t>((q >> 17) & 0x1FFFFu));
+  atomicAdd(c + 2 * nb + b, static_cast<uint32_t>(q >> 34));
+}
+__device__ __forceinline__ unsigned long long bin_mass(const uint32_t* c, int nb, int b) {
+  return static_cast<unsigned long long>(c[b]) + (static_cast<unsigned long long>(c[nb + b]) << 17) +
+         (static_cast<unsigned long long>(c[2 * nb + b]) << 34);
+}
+// per row: pow2ceil(T_n) keys, the bins, T_n flags, the forced-column bits
+__host__ __device__ inline size_t forced_bytes(int T_n) { return static_cast<size_t>((T_n + 127) / 128) * 16; }
 __host__ __device__ inline size_t row_smem_bytes(int T_n) {
-  return static_cast<size_t>(pow2ceil(T_n)) * 8 + kNB * 8 + ((T_n + 15) / 16) * 16;
+  return static_cast<size_t>(pow2ceil(T_n)) * 8 + 16 * kNB + ((T_n + 15) / 16) * 16 +
+         forced_bytes(T_n);
 }
 
 __device__ __forceinline__ double warp_max(double v) {
@@ -251,23 +274,75 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // always selected (guard).  ukey: the keys, entry j at ukey[j] (room for
 // pow2ceil(T_n) keys), overwritten: the boundary bin is compacted in place to
 // ukey[0, m) and sorted there; bsum: NB bin sums; flag: [T_n].
+template <int NB, int SUB = 8>
 __device__ __forceinline__ int bin_of(uint64_t key, int emax) {
+  constexpr int SB = SUB == 8 ? 3 : 5, NBIN = NB / SUB;   // binades covered
   const int e = static_cast<int>(key >> 52) & 0x7FF;
   const int db = emax - e;
-  if (db >= kNB / 8) return kNB - 1;
-  return db * 8 + (7 - static_cast<int>((key >> 49) & 7u));
+  if (db >= NBIN) return NB - 1;
+  return db * SUB + (SUB - 1 - static_cast<int>((key >> (52 - SB)) & (SUB - 1)));
 }
 // q_j = floor(e_j 2^sc): the largest entry (e_max = 1, emax its exponent)
-// lands in [2^52, 2^53) unless T_n * 2^(52 + 1) could overflow the 64-bit sum,
+// lands in [2^50, 2^51) unless T_n * 2^51 could overflow the 64-bit sum,
 // then sc drops to 63 - ceil(log2 T_n) (T_n <= 2^14: sc >= 49; entries below
 // 2^-sc of the max become 0 -- a cumulative error <= T_n 2^-sc, far inside
 // the 1e-6 band)
 __device__ __forceinline__ int fixed_point_scale(int emax, int T_n) {
   int lg = 0;
   while ((1 << lg) < T_n) ++lg;
-  return min(52 - (emax - 1023), 63 - lg);
+  return min(50 - (emax - 1023), 63 - lg);
 }
-__device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t* flag, int T_n,
+// The boundary bin over NB bins (warp-parallel, NB/32 bins per lane in
+// order): the first bin whose cumulative mass exceeds thr, and the mass of
+// the bins before it; NB when none does.
+template <int NB>
+__device__ __forceinline__ int boundary_bin(const uint32_t* c, double thr, int lane,
+                                            unsigned long long& a_star) {
+  constexpr int PER = NB / 32;
+  unsigned long long lsum = 0;
+#pragma unroll 8
+  for (int u = 0; u < PER; ++u) lsum += bin_mass(c, NB, lane * PER + u);
+  unsigned long long incl = lsum;
+#pragma unroll 8
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  unsigned long long above = incl - lsum;   // mass of the bins before this lane's first
+  int bstar = NB;
+  unsigned long long as = 0;
+#pragma unroll 8
+  for (int u = 0; u < PER; ++u) {
+    const int b = lane * PER + u;
+    const unsigned long long nxt = above + bin_mass(c, NB, b);
+    if (bstar == NB && static_cast<double>(nxt) > thr) { bstar = b; as = above; }
+    above = nxt;
+  }
+  int bmin = bstar;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+  const unsigned int owner = __ballot_sync(0xffffffffu, bstar == bmin && bmin < NB);
+  a_star = (bmin < NB) ? __shfl_sync(0xffffffffu, as, __ffs(owner) - 1) : 0ull;
+  return bmin;
+}
+// descending bitonic sort of one 64-bit key per lane across a warp
+__device__ __forceinline__ uint64_t warp_sort_desc(uint64_t k, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int st = size >> 1; st > 0; st >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, k, st);
+      const bool desc = ((lane & size) == 0);      // this lane's block sorts descending
+      const bool lower = ((lane & st) == 0);
+      // keep the larger on the lower lane of a descending block
+      const bool take_max = (desc == lower);
+      k = take_max ? max(k, o) : min(k, o);
+    }
+  }
+  return k;
+}
+
+__device__ void topcdf_binned(uint64_t* ukey, uint32_t* bins, uint8_t* flag, int T_n,
                               double tau, int lane) {
   auto kix = [](int j) { return j; };
   uint64_t* list = ukey;
@@ -278,7 +353,7 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t*
   for (int o = 16; o > 0; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
   const int emax = static_cast<int>(kmax >> 52) & 0x7FF;
   const int sc = fixed_point_scale(emax, T_n);
-  for (int b = lane; b < kNB; b += 32) bsum[b] = 0ull;
+  for (int b = lane; b < 3 * kNB; b += 32) bins[b] = 0u;
   __syncwarp();
   // the catch-all bin (>= 32 binades below the max: most entries of a
   // peaked row) is summed in registers -- 32-way atomic conflicts otherwise
@@ -287,43 +362,19 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t*
   for (int j = lane; j < T_n; j += 32) {
     const uint64_t k = ukey[kix(j)];
     const unsigned long long qj = __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale);
-    const int b = bin_of(k, emax);
+    const int b = bin_of<kNB>(k, emax);
     if (b == kNB - 1) q_last += qj;
-    else if (qj) atomicAdd(&bsum[b], qj);
+    else if (qj) bin_add(bins, kNB, b, qj);
     part += qj;
   }
   const unsigned long long total = warp_sum_u64(part);
   q_last = warp_sum_u64(q_last);
   __syncwarp();
-  if (lane == 0) bsum[kNB - 1] += q_last;
+  if (lane == 0) bin_add(bins, kNB, kNB - 1, q_last);
   __syncwarp();
   const double thr = (tau >= 1.0) ? INFINITY : tau * static_cast<double>(total);
-  // boundary bin: lane-parallel prefix over the NB bins (8 per lane, in order)
-  unsigned long long lsum = 0;
-#pragma unroll
-  for (int u = 0; u < kNB / 32; ++u) lsum += bsum[lane * (kNB / 32) + u];
-  unsigned long long incl = lsum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  unsigned long long above = incl - lsum;   // mass of bins before this lane's first
-  int bstar = kNB;
-  unsigned long long a_star = 0;
-#pragma unroll
-  for (int u = 0; u < kNB / 32; ++u) {
-    const int b = lane * (kNB / 32) + u;
-    const unsigned long long nxt = above + bsum[b];
-    if (bstar == kNB && static_cast<double>(nxt) > thr) { bstar = b; a_star = above; }
-    above = nxt;
-  }
-  // the first such bin over the warp
-  int bmin = bstar;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
-  const unsigned int owner = __ballot_sync(0xffffffffu, bstar == bmin && bmin < kNB);
-  if (bmin < kNB) a_star = __shfl_sync(0xffffffffu, a_star, __ffs(owner) - 1);
+  unsigned long long a_star;
+  const int bmin = boundary_bin<kNB>(bins, thr, lane, a_star);
   // flags outside the boundary bin; compact the boundary bin's keys in place
   // (write index m + rank <= j0 + lane <= kix(j0 + lane): never ahead of an
   // unread key, and the reads of a chunk precede its writes)
@@ -331,7 +382,7 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t*
   for (int j0 = 0; j0 < T_n; j0 += 32) {
     const int j = j0 + lane;
     const uint64_t k = (j < T_n) ? ukey[kix(j)] : 0ull;
-    const int b = (j < T_n) ? bin_of(k, emax) : kNB;
+    const int b = (j < T_n) ? bin_of<kNB>(k, emax) : kNB;
     const bool inb = (j < T_n) && (b == bmin);
     if (j < T_n) flag[j] = (b < bmin) ? 1 : 0;
     const unsigned int bal = __ballot_sync(0xffffffffu, inb);
@@ -340,14 +391,63 @@ __device__ void topcdf_binned(uint64_t* ukey, unsigned long long* bsum, uint8_t*
     m += __popc(bal);
     __syncwarp();
   }
-  if (bmin < kNB) {
+  // radix refinement of the boundary bin by 8 key bits per level (ordered
+  // in-place compaction of the crossing sub-bin) down to <= 32 entries
+  unsigned long long above = a_star;
+  int shift = 52 - 3 - 8;                       // key bits 48..41 first
+  int bcur = bmin;
+  while (bcur < kNB && m > 32 && shift >= 0) {
+    for (int b = lane; b < 4 * kNB; b += 32) bins[b] = 0u;
+    __syncwarp();
+    for (int t = lane; t < m; t += 32) {
+      const uint64_t k = list[t];
+      const int d = 255 - static_cast<int>((k >> shift) & 255u);
+      const unsigned long long q = __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale);
+      if (q) bin_add(bins, kNB, d, q);
+      atomicAdd(bins + 3 * kNB + d, 1u);
+    }
+    __syncwarp();
+    unsigned long long as;
+    bcur = boundary_bin<kNB>(bins, thr - static_cast<double>(above), lane, as);
+    above += as;
+    int mm = 0;
+    for (int t0 = 0; t0 < m; t0 += 32) {
+      const int t = t0 + lane;
+      const uint64_t k = (t < m) ? list[t] : 0ull;
+      const int d = 255 - static_cast<int>((k >> shift) & 255u);
+      if (t < m) flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (d < bcur) ? 1 : 0;
+      const bool inb = (t < m) && (d == bcur);
+      const unsigned int bal = __ballot_sync(0xffffffffu, inb);
+      __syncwarp();
+      if (inb) list[mm + __popc(bal & ((1u << lane) - 1u))] = k;
+      mm += __popc(bal);
+      __syncwarp();
+    }
+    m = mm;
+    shift -= 8;
+  }
+  if (bcur < kNB && m <= 32) {
+    // <= 32 boundary entries: order in registers, scan from `above`
+    uint64_t k = (lane < m) ? list[lane] : 0ull;
+    k = warp_sort_desc(k, lane);
+    unsigned long long qv =
+        (lane < m) ? __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale) : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, qv, o);
+      if (lane >= o) qv += y;
+    }
+    __syncwarp();
+    if (lane < m)
+      flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (static_cast<double>(above + qv) <= thr) ? 1 : 0;
+  } else if (bcur < kNB) {
     int n2 = 2;
     while (n2 < m) n2 <<= 1;
     for (int t = m + lane; t < n2; t += 32) list[t] = 0ull;
     __syncwarp();
     sort_desc_n(list, n2, lane);
     // sequential scan of the bin (in chunks of 32, integer prefix sums)
-    unsigned long long carry = a_star;
+    unsigned long long carry = above;
     for (int t0 = 0; t0 < m; t0 += 32) {
       const int t = t0 + lane;
       const uint64_t k = (t < m) ? list[t] : 0ull;
@@ -385,8 +485,10 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   unsigned char* base_w = smem + wid * per_warp;
   uint64_t* ukey = reinterpret_cast<uint64_t*>(base_w);
   double* key = reinterpret_cast<double*>(ukey);
-  unsigned long long* bsum = reinterpret_cast<unsigned long long*>(base_w + static_cast<size_t>(T_n) * 8);
-  uint8_t* flag = base_w + static_cast<size_t>(T_n) * 8 + kNB * 8;
+  const size_t nk = static_cast<size_t>(pow2ceil(T_n));
+  uint32_t* bins = reinterpret_cast<uint32_t*>(base_w + nk * 8);         // [4][kNB]
+  uint8_t* flag = base_w + nk * 8 + 16 * kNB;
+  uint32_t* forced = reinterpret_cast<uint32_t*>(flag + ((T_n + 15) / 16) * 16);   // s_k < theta
 
   const int i = row % T_m, bhq = row / T_m;
   const int hq = bhq % Hq, b = bhq / Hq;
@@ -402,7 +504,8 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   // them would otherwise serialise one load latency per 32 entries)
   constexpr int kLoadBatch = 8;
   double mx = -INFINITY;
-  for (int j0 = lane; j0 < T_n; j0 += 32 * kLoadBatch) {
+  for (int jb = 0; jb < T_n; jb += 32 * kLoadBatch) {     // warp-uniform bound (ballots below)
+    const int j0 = jb + lane;
     double sv[kLoadBatch], kv[kLoadBatch];
 #pragma unroll
     for (int u = 0; u < kLoadBatch; ++u) {
@@ -413,8 +516,11 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
 #pragma unroll
     for (int u = 0; u < kLoadBatch; ++u) {
       const int j = j0 + 32 * u;
+      const bool fc = (j < n_live) && (kv[u] < theta);
+      const unsigned int fb = __ballot_sync(0xffffffffu, fc);
+      if (lane == 0 && j - lane < T_n) forced[(j - lane) >> 5] = fb;
       if (j < T_n) {
-        const double s = (kv[u] < theta) ? -INFINITY : sv[u];
+        const double s = fc ? -INFINITY : sv[u];
         key[j] = s;
         mx = fmax(mx, s);
       }
@@ -439,7 +545,7 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
                 static_cast<uint64_t>(kIdxMask - j);
     }
     __syncwarp();
-    topcdf_binned(ukey, bsum, flag, T_n, tau, lane);
+    topcdf_binned(ukey, bins, flag, T_n, tau, lane);
   }
 
   // ---- forcing (Eq. 5), flagged rows, causal live AND + diagonal guard ----
@@ -453,7 +559,7 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
     bool f = false;
     if (j < T_n) {
       f = flagged ? true : (flag[j] != 0);
-      if (row_fix || (j < n_live && k_sim[kbase + j] < theta)) f = true;
+      if (row_fix || ((forced[j >> 5] >> (j & 31)) & 1u)) f = true;
       if (causal) {
         if (j >= n_live) f = false;
         if (j == guard) f = true;
@@ -479,8 +585,11 @@ constexpr int kCtaWarps = 4;
 constexpr int kCtaThreads = kCtaWarps * 32;
 constexpr int kListCap = 1024;   // boundary entries gathered outside the key array
 
+// keys, bins (3 mass chunks + a count per bin), two boundary lists, flags,
+// forced-column bits
 __host__ __device__ inline size_t cta_row_smem_bytes(int T_n) {
-  return static_cast<size_t>(pow2ceil(T_n)) * 8 + kNB * 8 + kListCap * 8 + ((T_n + 15) / 16) * 16;
+  return static_cast<size_t>(pow2ceil(T_n)) * 8 + 4 * 4 * kNBCta + 2 * kListCap * 8 +
+         ((T_n + 15) / 16) * 16 + forced_bytes(T_n);
 }
 
 __device__ __forceinline__ double block_max(double v, double* red) {
@@ -503,7 +612,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[kCtaWarps];
   __shared__ unsigned long long red_u[kCtaWarps];
-  __shared__ int s_info[4];                 // bmin, m (boundary entries), list overflow
+  __shared__ int s_info[4];                 // bmin, m (boundary entries), refinement bin, count
   __shared__ unsigned long long s_astar;
   __shared__ int s_wcount[kCtaWarps];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -511,9 +620,11 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   uint64_t* ukey = reinterpret_cast<uint64_t*>(smem);
   double* key = reinterpret_cast<double*>(ukey);
   const size_t nk = static_cast<size_t>(pow2ceil(T_n));
-  unsigned long long* bsum = reinterpret_cast<unsigned long long*>(smem + nk * 8);
-  uint64_t* list = reinterpret_cast<uint64_t*>(smem + nk * 8 + kNB * 8);
-  uint8_t* flag = smem + nk * 8 + kNB * 8 + kListCap * 8;
+  uint32_t* bins = reinterpret_cast<uint32_t*>(smem + nk * 8);           // [4][kNBCta]
+  uint64_t* list = reinterpret_cast<uint64_t*>(smem + nk * 8 + 16 * kNBCta);
+  uint64_t* list2 = list + kListCap;
+  uint8_t* flag = smem + nk * 8 + 16 * kNBCta + 2 * kListCap * 8;
+  uint32_t* forced = reinterpret_cast<uint32_t*>(flag + ((T_n + 15) / 16) * 16);   // s_k < theta
 
   const int i = row % T_m, bhq = row / T_m;
   const int hq = bhq % Hq, b = bhq / Hq;
@@ -525,7 +636,8 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   // ---- S^ row with the -inf columns (fixed K blocks, causally dead) ----
   constexpr int kLoadBatch = 4;
   double mx = -INFINITY;
-  for (int j0 = tid; j0 < T_n; j0 += kCtaThreads * kLoadBatch) {
+  for (int jb = 0; jb < T_n; jb += kCtaThreads * kLoadBatch) {   // uniform bound (ballots)
+    const int j0 = jb + tid;
     double sv[kLoadBatch], kv[kLoadBatch];
 #pragma unroll
     for (int u = 0; u < kLoadBatch; ++u) {
@@ -536,14 +648,17 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
 #pragma unroll
     for (int u = 0; u < kLoadBatch; ++u) {
       const int j = j0 + kCtaThreads * u;
+      const bool fc = (j < n_live) && (kv[u] < theta);
+      const unsigned int fb = __ballot_sync(0xffffffffu, fc);
+      if (lane == 0 && j - lane < T_n) forced[(j - lane) >> 5] = fb;
       if (j < T_n) {
-        const double sj = (kv[u] < theta) ? -INFINITY : sv[u];
+        const double sj = fc ? -INFINITY : sv[u];
         key[j] = sj;
         mx = fmax(mx, sj);
       }
     }
   }
-  for (int t = tid; t < kNB; t += kCtaThreads) bsum[t] = 0ull;
+  for (int t = tid; t < 3 * kNBCta; t += kCtaThreads) bins[t] = 0u;
   mx = block_max(mx, red);
   const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
 
@@ -574,47 +689,25 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
     for (int j = tid; j < T_n; j += kCtaThreads) {
       const uint64_t k = ukey[j];
       const unsigned long long qj = __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale);
-      const int bb = bin_of(k, emax);
-      if (bb == kNB - 1) q_last += qj;              // catch-all bin in registers
-      else if (qj) atomicAdd(&bsum[bb], qj);
+      const int bb = bin_of<kNBCta>(k, emax);
+      if (bb == kNBCta - 1) q_last += qj;           // catch-all bin in registers
+      else if (qj) bin_add(bins, kNBCta, bb, qj);
       qpart += qj;
     }
     qpart = warp_sum_u64(qpart);
     q_last = warp_sum_u64(q_last);
-    if (lane == 0 && q_last) atomicAdd(&bsum[kNB - 1], q_last);
-    __syncthreads();                                 // bsum complete; red_u reuse
+    if (lane == 0 && q_last) bin_add(bins, kNBCta, kNBCta - 1, q_last);
+    __syncthreads();                                 // bins complete; red_u reuse
     if (lane == 0) red_u[wid] = qpart;
     __syncthreads();
     unsigned long long qtotal = 0;
 #pragma unroll
     for (int w = 0; w < kCtaWarps; ++w) qtotal += red_u[w];
     const double thr = (tau >= 1.0) ? INFINITY : tau * static_cast<double>(qtotal);
-    // boundary bin by warp 0 (lane-parallel prefix over the NB bins)
+    // boundary bin by warp 0 (lane-parallel prefix over the bins)
     if (wid == 0) {
-      unsigned long long lsum = 0;
-#pragma unroll
-      for (int u = 0; u < kNB / 32; ++u) lsum += bsum[lane * (kNB / 32) + u];
-      unsigned long long incl = lsum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      unsigned long long above = incl - lsum;
-      int bstar = kNB;
-      unsigned long long a_star = 0;
-#pragma unroll
-      for (int u = 0; u < kNB / 32; ++u) {
-        const int bb = lane * (kNB / 32) + u;
-        const unsigned long long nxt = above + bsum[bb];
-        if (bstar == kNB && static_cast<double>(nxt) > thr) { bstar = bb; a_star = above; }
-        above = nxt;
-      }
-      int bmin = bstar;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
-      const unsigned int owner = __ballot_sync(0xffffffffu, bstar == bmin && bmin < kNB);
-      if (bmin < kNB) a_star = __shfl_sync(0xffffffffu, a_star, __ffs(owner) - 1);
+      unsigned long long a_star;
+      const int bmin = boundary_bin<kNBCta>(bins, thr, lane, a_star);
       if (lane == 0) {
         s_info[0] = bmin;
         s_info[1] = 0;
@@ -628,7 +721,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
     for (int j0 = wid * 32; j0 < T_n; j0 += kCtaThreads) {
       const int j = j0 + lane;
       const uint64_t k = (j < T_n) ? ukey[j] : 0ull;
-      const int bb = (j < T_n) ? bin_of(k, emax) : kNB;
+      const int bb = (j < T_n) ? bin_of<kNBCta>(k, emax) : kNBCta;
       const bool inb = (j < T_n) && (bb == bmin);
       if (j < T_n) flag[j] = (bb < bmin) ? 1 : 0;
       const unsigned int bal = __ballot_sync(0xffffffffu, inb);
@@ -639,9 +732,69 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
       if (inb && pos < kListCap) list[pos] = k;
     }
     __syncthreads();
-    const int m = s_info[1];
-    if (wid == 0 && bmin < kNB) {
-      uint64_t* lst = list;
+    int m = s_info[1];
+    // radix refinement of the boundary bin (it fits the lists): histogram its
+    // entries by the next 8 key bits, keep the sub-bins above the crossing
+    // one, recurse into that sub-bin until <= 32 entries remain, which warp 0
+    // orders in registers and scans (a large boundary bin -- a smooth P^
+    // near the cut -- made the warp-0 bitonic sort the critical path)
+    unsigned long long above = s_astar;
+    uint64_t* la = list;
+    uint64_t* lb = list2;
+    int shift = 52 - 3 - 8;                     // key bits 48..41 first
+    while (bmin < kNBCta && m > 32 && m <= kListCap && shift >= 0) {
+      for (int t = tid; t < 4 * kNBCta; t += kCtaThreads) bins[t] = 0u;
+      __syncthreads();
+      for (int t = tid; t < m; t += kCtaThreads) {
+        const uint64_t k = la[t];
+        const int d = 255 - static_cast<int>((k >> shift) & 255u);
+        const unsigned long long q = __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale);
+        if (q) bin_add(bins, kNBCta, d, q);
+        atomicAdd(bins + 3 * kNBCta + d, 1u);
+      }
+      __syncthreads();
+      if (wid == 0) {
+        unsigned long long as;
+        const int b2 = boundary_bin<kNBCta>(bins, thr - static_cast<double>(above), lane, as);
+        if (lane == 0) {
+          s_info[2] = b2;
+          s_info[3] = 0;
+          s_astar = as;
+        }
+      }
+      __syncthreads();
+      const int b2 = s_info[2];
+      above += s_astar;
+      for (int t = tid; t < m; t += kCtaThreads) {
+        const uint64_t k = la[t];
+        const int d = 255 - static_cast<int>((k >> shift) & 255u);
+        flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (d < b2) ? 1 : 0;
+        if (d == b2) lb[atomicAdd(&s_info[3], 1)] = k;
+      }
+      __syncthreads();
+      m = s_info[3];
+      uint64_t* tmp = la;
+      la = lb;
+      lb = tmp;
+      shift -= 8;
+      __syncthreads();                          // s_info / s_astar reuse
+    }
+    if (wid == 0 && bmin < kNBCta && m <= 32) {
+      // <= 32 boundary entries: order in registers, scan from `above`
+      uint64_t k = (lane < m) ? la[lane] : 0ull;
+      k = warp_sort_desc(k, lane);
+      unsigned long long qv =
+          (lane < m) ? __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale) : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, qv, o);
+        if (lane >= o) qv += y;
+      }
+      if (lane < m)
+        flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (static_cast<double>(above + qv) <= thr) ? 1 : 0;
+    } else if (wid == 0 && bmin < kNBCta) {
+      const unsigned long long carry0 = above;
+      uint64_t* lst = la;
       if (m > kListCap) {
         // rare (a huge boundary bin, e.g. near-uniform P^): warp 0 alone
         // compacts the bin in place in the key array, as topcdf_binned does
@@ -650,7 +803,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
         for (int j0 = 0; j0 < T_n; j0 += 32) {
           const int j = j0 + lane;
           const uint64_t k = (j < T_n) ? ukey[j] : 0ull;
-          const bool inb = (j < T_n) && (bin_of(k, emax) == bmin);
+          const bool inb = (j < T_n) && (bin_of<kNBCta>(k, emax) == bmin);
           const unsigned int bal = __ballot_sync(0xffffffffu, inb);
           __syncwarp();
           if (inb) lst[mm + __popc(bal & ((1u << lane) - 1u))] = k;
@@ -663,7 +816,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
       for (int t = m + lane; t < n2; t += 32) lst[t] = 0ull;
       __syncwarp();
       sort_desc_n(lst, n2, lane);
-      unsigned long long carry = s_astar;
+      unsigned long long carry = carry0;
       for (int t0 = 0; t0 < m; t0 += 32) {
         const int t = t0 + lane;
         const uint64_t k = (t < m) ? lst[t] : 0ull;
@@ -693,7 +846,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   const int c0 = wid * ch, c1 = min(T_n, c0 + ch);
   auto kept = [&](int j) {
     bool f = flagged ? true : (flag[j] != 0);
-    if (row_fix || (j < n_live && k_sim[kbase + j] < theta)) f = true;
+    if (row_fix || ((forced[j >> 5] >> (j & 31)) & 1u)) f = true;
     if (causal) {
       if (j >= n_live) f = false;
       if (j == guard) f = true;
@@ -740,6 +893,7 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
   k_shat_dmma<D><<<g1, kGemmThreads, smem_g, stream>>>(q_pooled, k_pooled, s.Hq, s.Hkv, T_m, T_n,
                                                         s.N, s.bq, s.bk, s.causal, shat);
   const int rows = s.B * s.Hq * T_m;
+  const double tau_d = static_cast<double>(tau), theta_d = static_cast<double>(theta);
   // long rows: one CTA of kCtaWarps warps per row (occupancy); short rows:
   // one warp per row, up to kMaxRowWarps rows per CTA
   if (T_n > cta_row_min_tn()) {
@@ -748,8 +902,8 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
                              static_cast<int>(smem_c));
     if (e != cudaSuccess) return e;
     k_topcdf_cta<D><<<rows, kCtaThreads, smem_c, stream>>>(
-        shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, s.bq, s.bk, s.causal,
-        static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
+        shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, s.bq, s.bk, s.causal, tau_d, theta_d,
+        mask, lut, cnt);
     return cudaGetLastError();
   }
   // rows per CTA: up to kMaxRowWarps, as many as fit the shared memory
@@ -761,8 +915,8 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
                            static_cast<int>(smem_r));
   if (e != cudaSuccess) return e;
   k_topcdf_rows<D><<<(rows + warps - 1) / warps, warps * 32, smem_r, stream>>>(
-      shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, s.bq, s.bk, s.causal,
-      static_cast<double>(tau), static_cast<double>(theta), mask, lut, cnt);
+      shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, s.bq, s.bk, s.causal, tau_d, theta_d,
+      mask, lut, cnt);
   return cudaGetLastError();
 }
 
