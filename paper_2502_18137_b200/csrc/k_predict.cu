@@ -765,11 +765,17 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
       __syncthreads();
       const int b2 = s_info[2];
       above += s_astar;
-      for (int t = tid; t < m; t += kCtaThreads) {
-        const uint64_t k = la[t];
+      for (int t0 = wid * 32; t0 < m; t0 += kCtaThreads) {   // warp-aggregated gather
+        const int t = t0 + lane;
+        const uint64_t k = (t < m) ? la[t] : 0ull;
         const int d = 255 - static_cast<int>((k >> shift) & 255u);
-        flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (d < b2) ? 1 : 0;
-        if (d == b2) lb[atomicAdd(&s_info[3], 1)] = k;
+        if (t < m) flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (d < b2) ? 1 : 0;
+        const bool inb = (t < m) && (d == b2);
+        const unsigned int bal = __ballot_sync(0xffffffffu, inb);
+        int pos = 0;
+        if (lane == 0 && bal) pos = atomicAdd(&s_info[3], __popc(bal));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (inb) lb[pos + __popc(bal & ((1u << lane) - 1u))] = k;
       }
       __syncthreads();
       m = s_info[3];
@@ -853,22 +859,25 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
     }
     return f;
   };
+  // pass 1: the kept bits of each 32-entry word (overwriting that word's
+  // forced bits, already read by every lane before the ballot), the mask
+  // and the warp's count; pass 2: the LUT from the words
   int wc = 0;
   for (int j0 = c0; j0 < c1; j0 += 32) {
     const int j = j0 + lane;
     const bool f = (j < c1) && kept(j);
     if (j < c1 && mrow) mrow[j] = f ? 1 : 0;
-    wc += __popc(__ballot_sync(0xffffffffu, f));
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) forced[j0 >> 5] = bal;
+    wc += __popc(bal);
   }
   if (lane == 0) s_wcount[wid] = wc;
   __syncthreads();
   int base = 0;
   for (int w = 0; w < wid; ++w) base += s_wcount[w];
   for (int j0 = c0; j0 < c1; j0 += 32) {
-    const int j = j0 + lane;
-    const bool f = (j < c1) && kept(j);
-    const unsigned bal = __ballot_sync(0xffffffffu, f);
-    if (f) lrow[base + __popc(bal & ((1u << lane) - 1u))] = j;
+    const unsigned bal = forced[j0 >> 5];
+    if ((bal >> lane) & 1u) lrow[base + __popc(bal & ((1u << lane) - 1u))] = j0 + lane;
     base += __popc(bal);
   }
   if (tid == 0) {
