@@ -222,9 +222,10 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
 __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                            uint32_t idesc, uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -243,9 +244,10 @@ __device__ __forceinline__ uint32_t pack_e4m3x2(float lo, float hi) {
 __device__ __forceinline__ void mma_f8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                           uint32_t idesc, uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -391,16 +393,19 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
 
   if (warp == WARP_LOAD) {
     // ============================ TMA producer ============================
-    if (lane == 0 && n_tiles > 0) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      mbar_arrive_expect_tx(q_full, L::Q_BYTES);
+    // (the whole warp runs the loop, one elected lane issues: see sm100.cuh)
+    if (n_tiles > 0) {
+      if (lane == 0) {
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+      }
+      mbar_arrive_expect_tx_ew(q_full, L::Q_BYTES);
       if (QK16) {
 #pragma unroll
-        for (int h = 0; h < D / 64; ++h) tma_load_3d(sQ + h * L::Q_ATOM, &tmQ, q_full, h * 64, i * BQ, bhq);
+        for (int h = 0; h < D / 64; ++h) tma_load_3d_ew(sQ + h * L::Q_ATOM, &tmQ, q_full, h * 64, i * BQ, bhq);
       } else {
-        tma_load_3d(sQ, &tmQ, q_full, 0, i * BQ, bhq);
+        tma_load_3d_ew(sQ, &tmQ, q_full, 0, i * BQ, bhq);
       }
       int j_next = __ldg(lut_row);
       for (int t = 0; t < n_tiles; ++t) {
@@ -408,13 +413,13 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         if (t + 1 < n_tiles) j_next = __ldg(lut_row + t + 1);
         const int ks = t % KST;
         mbar_wait(s_full + ks, ((t / KST) & 1) ^ 1);     // QK(t - KST) done: slot free
-        mbar_arrive_expect_tx(k_full + ks, L::K_BYTES);
+        mbar_arrive_expect_tx_ew(k_full + ks, L::K_BYTES);
         if (QK16) {
 #pragma unroll
           for (int h = 0; h < D / 64; ++h)
-            tma_load_3d(sK + ks * L::K_BYTES + h * L::K_ATOM, &tmK, k_full + ks, h * 64, j * BK, bkv);
+            tma_load_3d_ew(sK + ks * L::K_BYTES + h * L::K_ATOM, &tmK, k_full + ks, h * 64, j * BK, bkv);
         } else {
-          tma_load_3d(sK + ks * L::K_BYTES, &tmK, k_full + ks, 0, j * BK, bkv);
+          tma_load_3d_ew(sK + ks * L::K_BYTES, &tmK, k_full + ks, 0, j * BK, bkv);
         }
         const int vs = t % VST;
         // V slot of tile t - VST is free once P~V(t - VST) is done, i.e. once
@@ -426,14 +431,15 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           const int u = t - VST + L::NSB;
           mbar_wait(s_full + u % KST, (u / KST) & 1);
         }
-        mbar_arrive_expect_tx(v_full + vs, L::V_BYTES);
-        if (kVtTiled && !PV8) tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, 0, j * D, bkv);
-        else tma_load_3d(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
+        mbar_arrive_expect_tx_ew(v_full + vs, L::V_BYTES);
+        if (kVtTiled && !PV8) tma_load_3d_ew(sV + vs * L::V_BYTES, &tmV, v_full + vs, 0, j * D, bkv);
+        else tma_load_3d_ew(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
       }
     }
   } else if (warp == WARP_MMA) {
     // ============================ MMA issuer ==============================
-    if (lane == 0 && n_tiles > 0) {
+    // (the whole warp runs the loop, one elected lane issues: see sm100.cuh)
+    if (n_tiles > 0) {
       constexpr uint32_t IDESC_QK =
           QK16 ? (F16 ? idesc_f16(BQ, BK) : idesc_bf16(BQ, BK)) : idesc_i8(BQ, BK);
       // (kind::f8f6f4 with E4M3 A/B and fp32 D has the f16 field values)
@@ -478,7 +484,7 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         // is issued after P~V(t-1)) while that tile exists, else on o_tail, as
         // does the epilogue -- one tcgen05.commit (~44 issue cycles) less per
         // tile
-        if (u + NSB >= n_tiles) tc_commit(o_tail + (u - max(0, n_tiles - NSB)));
+        if (u + NSB >= n_tiles) tc_commit_ew(o_tail + (u - max(0, n_tiles - NSB)));
       };
       // QK(t) into S[t % NSB]: issued right after P~V(t - NSB), the previous
       // reader of that buffer (tcgen05.mma from one thread execute in issue
@@ -497,23 +503,23 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
           // the next atom (fp32 S accumulators)
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
-            mma_f16(tS0 + sb * BK, dQ + (((kk >> 2) * L::Q_ATOM + (kk & 3) * 32) >> 4),
+            mma_f16_ew(tS0 + sb * BK, dQ + (((kk >> 2) * L::Q_ATOM + (kk & 3) * 32) >> 4),
                     dK + (((kk >> 2) * L::K_ATOM + (kk & 3) * 32) >> 4), IDESC_QK, kk > 0 ? 1u : 0u);
         } else {
           if (L::BIAS)   // S := 1.5*2^23 (fp32 bits), then += acc as int32
-            mma_f16(tS0 + sb * BK, dCA, dCB, IDESC_BIAS, 0u);
+            mma_f16_ew(tS0 + sb * BK, dCA, dCB, IDESC_BIAS, 0u);
 #pragma unroll
           for (int kk = 0; kk < D / 32; ++kk)       // K = 32 per kind::i8 MMA (32 B)
-            mma_i8(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, (L::BIAS || kk > 0) ? 1u : 0u);
+            mma_i8_ew(tS0 + sb * BK, dQ + 2 * kk, dK + 2 * kk, IDESC_QK, (L::BIAS || kk > 0) ? 1u : 0u);
         }
-        tc_commit(s_full + ks);
+        tc_commit_ew(s_full + ks);
       };
       for (int t = 0; t < NSB - 1 && t < n_tiles; ++t) issue_qk(t);
       for (int t = 0; t < n_tiles; ++t) {
         if (t + NSB - 1 < n_tiles) issue_qk(t + NSB - 1);
         do_pv(t);
       }
-      if (p.counters) atomicAdd(p.counters + bhq * 3 + 2, issued);
+      if (p.counters && lane == 0) atomicAdd(p.counters + bhq * 3 + 2, issued);
     }
   } else {
     // ============================ softmax warps ===========================
