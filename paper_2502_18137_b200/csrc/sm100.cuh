@@ -29,6 +29,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // Block until the phase with parity `parity` of `bar` has completed.  The
 // suspend-time hint lets the waiting warp sleep in hardware instead of
 // re-issuing try_wait (spinning warps steal issue slots from the softmax).
+#ifndef SPARGE_BACKOFF_NS
+#define SPARGE_BACKOFF_NS 128
+#endif
 #ifndef SPARGE_WAIT_HINT
 #define SPARGE_WAIT_HINT 1
 #endif
@@ -48,6 +51,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}"
       ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 #endif
+}
+
+// Wait with a nanosleep back-off between polls, for a warp that runs ahead
+// of the pipeline (the TMA producer): a spinning try_wait loop there issued
+// ~20 % of the attention kernel's instructions on its SMSP (ncu r02),
+// issue slots the softmax warp sharing that SMSP needs.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  while (!done) {
+    __nanosleep(SPARGE_BACKOFF_NS);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  }
 }
 
 // ------------------------------------------------------------------ TMA
@@ -199,6 +223,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "tcgen05.st.sync.aligned.32x32b.x16.b32"
       " [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
       ::"r"(taddr), SPARGE_W8(0), SPARGE_W8(8)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+      ::"r"(taddr), SPARGE_W8(0)
       : "memory");
 }
 #undef SPARGE_W8
