@@ -400,6 +400,19 @@ def roofline_of(d, qk_exec, pv_slices, attn_ms, workload):
                          f"uses the nominal 4500/2250 TOPS mix ({sheet_peak:.0f})"}, bf16_peak
 
 
+def mufu_roofline_of(qk_exec, attn_ms, n_sm, clk_mhz):
+    """The attention kernel's second bound: every kept 128x64 tile
+    exponentiates its 8192 entries on the MUFU (ex2.approx, 16 per clock per
+    SM: scripts/ubench_mufu_*.cu), so exp2/s against 16 x SMs x the maximum
+    SM clock is the fraction of that pipe's peak."""
+    exps = qk_exec * 128.0 * 64.0
+    achieved = exps / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else 0.0
+    peak = 16.0 * n_sm * clk_mhz * 1e6 / 1e9
+    return {"bound": "mufu", "kernel": "k_sparse_attn", "achieved": achieved, "peak": peak,
+            "unit": "Gexp2/s", "frac": achieved / peak if peak else None,
+            "note": f"8192 ex2 per executed QK tile; peak = 16/clk/SM x {n_sm} SMs x {clk_mhz:.0f} MHz"}
+
+
 def hyper(cfg, name, triple):
     """tau/theta/lambda of a workload: the §3.6 tuner's values at the paper's
     bounds (inputs.TUNED, profiles/r02_f2_tuned.json) or the fixed R20 triple."""
@@ -506,6 +519,13 @@ def run_ours(args):
     c_loc = prob.bf.counters.cpu().numpy().astype(np.int64) if not prob.empty else np.zeros((1, 1, 3))
     roofline, bf16_peak = roofline_of(d, int(c_loc[0, :, 0].sum()), int(c_loc[0, :, 1].sum()),
                                       stages["attn_ms"], args.workload)
+    try:
+        sm_max = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+    except Exception:
+        sm_max = 1965.0
+    roofline_mufu = mufu_roofline_of(int(c_loc[0, :, 0].sum()), stages["attn_ms"],
+                                     torch.cuda.get_device_properties(dev).multi_processor_count,
+                                     sm_max)
     if world > 1 and args.shard == "heads":
         par = f"heads: kv-groups split over {world} ranks (no data-path collective)"
     elif world > 1:
@@ -532,6 +552,7 @@ def run_ours(args):
                         "note": "a0 index build on the host once per shape; the gather is "
                                 "fused into a1 / the V stage and the scatter into a3"},
         "roofline": roofline,
+        "roofline_mufu": roofline_mufu,
         "gpu_launches": (0 if prob.empty else LAUNCHES_PER_STEP) * K,
         "clocks": clk,
     }
