@@ -453,6 +453,11 @@ def measure_workload(name, args, world, rank, dev, flush, sync, K, W, dense=True
         std, _ = time_steps(prob, Kd, 1, flush, sync, tau=1.0, theta=-1.0, lam=-math.inf)
         dms = multigpu.max_over_ranks(float(std.sum(1).mean()), dev)
         out["dense_value"] = ops_total / (dms * 1e-3) / 1e12
+        # Table 3's overhead: prediction time over the FULL
+        # (dense) attention time -- the dense comparator's attention stage
+        dattn = float(std[:, 3].mean())
+        out["dense_attn_ms"] = dattn
+        out["predict_over_dense_attn"] = stages["predict_ms"] / dattn if dattn else None
         out["speedup"] = out["value"] / out["dense_value"]
         out["target_0.8/(1-s)"] = 0.8 / max(1e-9, 1.0 - out["sparsity"])
     del prob
@@ -576,9 +581,13 @@ def run_ours(args):
                             lam=-math.inf)
         dms = multigpu.max_over_ranks(float(std.sum(1).mean()), dev)
         dense_value = ops_total / (dms * 1e-3) / 1e12
+        dattn = float(std[:, 3].mean())
         result["dense"] = {"value": dense_value, "ms_per_step": dms,
+                           "attn_ms": dattn,
                            "speedup": value / dense_value,
                            "target_0.8/(1-s)": 0.8 / max(1e-9, 1.0 - sparsity)}
+        # Table 3's overhead: prediction over FULL attention
+        result["predict_over_dense_attn"] = stages["predict_ms"] / dattn if dattn else None
 
     # ---- the fixed R20 triple on the same inputs (round 1's headline) ----
     if args.triple == "tuned" and not prob.empty:
