@@ -42,4 +42,8 @@ for s in np.unique(sm):
     ends = np.sort(x)
     gaps.append(np.sum(np.maximum(0, e[2:] - ends[:len(e) - 2])))
 print(f"  SMs {len(busy)}; mean SM CTA-busy {np.mean(busy)/1e3:.1f} us (2 slots -> slot-time {np.mean(busy)/2e3:.1f} us of span {span/1e3:.1f})")
+starts = [entry[sm == s].min() - t0 for s in np.unique(sm)]
+fins = [exit_.max() - exit_[sm == s].max() for s in np.unique(sm)]
+print(f"  per SM: slot gaps between CTAs {np.mean(gaps)/2e3:.1f} us per slot, "
+      f"first entry after kernel start {np.mean(starts)/1e3:.1f} us, idle after its last CTA {np.mean(fins)/1e3:.1f} us")
 print(f"  last CTA exit minus median SM finish: {(exit_.max() - np.median([exit_[sm==s].max() for s in np.unique(sm)]))/1e3:.1f} us")
