@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 measurement pass: GPU suite, smoke, the default bench line (+ sweep, e2e, host baseline),
 # per-workload lines, the reference arm, an ncu launch list and full captures of the top kernels.
-O=gpurun_out/final
+O=gpurun_out/final2
 mkdir -p $O
 python -m pytest tests -m gpu -q --timeout 1500 > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
