@@ -688,7 +688,8 @@ def run_ours(args):
             single.step()
             torch.cuda.synchronize()
             result["multi_gpu"].update({
-                "gather": "NCCL all_gather of O (outside the timed region)",
+                "gather": f"{torch.distributed.get_backend().upper()} all_gather of O "
+                          "(outside the timed region)",
                 "o_bit_equal_to_single_gpu": bool(torch.equal(o_full, single.o)),
                 "max_abs_diff": float((o_full.float() - single.o.float()).abs().max())})
             del single
