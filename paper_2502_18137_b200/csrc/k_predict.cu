@@ -288,8 +288,7 @@ __device__ __forceinline__ int bin_of(uint64_t key, int emax) {
 // 2^-sc of the max become 0 -- a cumulative error <= T_n 2^-sc, far inside
 // the 1e-6 band)
 __device__ __forceinline__ int fixed_point_scale(int emax, int T_n) {
-  int lg = 0;
-  while ((1 << lg) < T_n) ++lg;
+  const int lg = T_n > 1 ? 32 - __clz(T_n - 1) : 0;     // ceil(log2 T_n)
   return min(50 - (emax - 1023), 63 - lg);
 }
 // The boundary bin over NB bins (warp-parallel, NB/32 bins per lane in
@@ -580,7 +579,9 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
 // (12.5 % occupancy, ncu r02_pred128k); a CTA per row keeps ~40 warps busy.
 // Streaming phases split j across the warps; reductions go through shared
 // memory in a fixed order (deterministic); the boundary bin (usually small)
-// is compacted, sorted and scanned by warp 0.
+// is compacted, sorted and scanned by warp 0.  The binning pass caches each
+// entry's bin (u8), so the gather and mask passes decide "bin < b*" without
+// the key; the boundary entries' decisions are bits set by the refinement.
 constexpr int kCtaWarps = 4;
 constexpr int kCtaThreads = kCtaWarps * 32;
 #ifndef SPARGE_LISTCAP
@@ -592,11 +593,11 @@ constexpr int kCtaThreads = kCtaWarps * 32;
 // vs 1024 (r02)
 constexpr int kListCap = SPARGE_LISTCAP;
 
-// keys, bins (3 mass chunks + a count per bin), two boundary lists, flags,
-// forced-column bits
+// keys, bins (3 mass chunks + a count per bin), two boundary lists, the
+// entries' bin indices, forced-column bits, boundary-decision bits
 __host__ __device__ inline size_t cta_row_smem_bytes(int T_n) {
   return static_cast<size_t>(pow2ceil(T_n)) * 8 + 4 * 4 * kNBCta + 2 * kListCap * 8 +
-         ((T_n + 15) / 16) * 16 + forced_bytes(T_n);
+         ((T_n + 15) / 16) * 16 + 2 * forced_bytes(T_n);
 }
 
 __device__ __forceinline__ double block_max(double v, double* red) {
@@ -630,8 +631,14 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   uint32_t* bins = reinterpret_cast<uint32_t*>(smem + nk * 8);           // [4][kNBCta]
   uint64_t* list = reinterpret_cast<uint64_t*>(smem + nk * 8 + 16 * kNBCta);
   uint64_t* list2 = list + kListCap;
-  uint8_t* flag = smem + nk * 8 + 16 * kNBCta + 2 * kListCap * 8;
-  uint32_t* forced = reinterpret_cast<uint32_t*>(flag + ((T_n + 15) / 16) * 16);   // s_k < theta
+  // bin of each entry (u8; kNBCta = 256 bins) -- pass 4 and the mask pass
+  // read it instead of recomputing bin_of from the key
+  uint8_t* ebin = smem + nk * 8 + 16 * kNBCta + 2 * kListCap * 8;
+  uint32_t* forced = reinterpret_cast<uint32_t*>(ebin + ((T_n + 15) / 16) * 16);   // s_k < theta
+  // kept bits of the boundary bin's entries (and the guard), set by the
+  // refinement / final scan; every other entry is kept iff its bin < bmin
+  uint32_t* dec = forced + forced_bytes(T_n) / 4;
+  static_assert(kNBCta == 256, "bin indices stored as u8");
 
   const int i = row % T_m, bhq = row / T_m;
   const int hq = bhq % Hq, b = bhq / Hq;
@@ -666,8 +673,11 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
     }
   }
   for (int t = tid; t < 3 * kNBCta; t += kCtaThreads) bins[t] = 0u;
+  for (int t = tid; t < static_cast<int>(forced_bytes(T_n) / 4); t += kCtaThreads) dec[t] = 0u;
   mx = block_max(mx, red);
   const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
+  int bmin = kNBCta;                         // entries of bins < bmin are kept
+  auto keep_bit = [&](int j) { atomicOr(dec + (j >> 5), 1u << (j & 31)); };
 
   if (!flagged) {
     // keys (bits of e = exp(S^ - max), low kIdxBits replaced by kIdxMask - j;
@@ -697,6 +707,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
       const uint64_t k = ukey[j];
       const unsigned long long qj = __double2ull_rz(__longlong_as_double(k & ~kIdxMask) * scale);
       const int bb = bin_of<kNBCta>(k, emax);
+      ebin[j] = static_cast<uint8_t>(bb);
       if (bb == kNBCta - 1) q_last += qj;           // catch-all bin in registers
       else if (qj) bin_add(bins, kNBCta, bb, qj);
       qpart += qj;
@@ -722,21 +733,19 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
       }
     }
     __syncthreads();
-    const int bmin = s_info[0];
-    // flags outside the boundary bin; the boundary entries gathered into
-    // `list` (order irrelevant: sorted below) while they fit kListCap
+    bmin = s_info[0];
+    // the boundary entries gathered into `list` (order irrelevant: sorted
+    // below) while they fit kListCap; the other entries are decided by bin
     for (int j0 = wid * 32; j0 < T_n; j0 += kCtaThreads) {
       const int j = j0 + lane;
-      const uint64_t k = (j < T_n) ? ukey[j] : 0ull;
-      const int bb = (j < T_n) ? bin_of<kNBCta>(k, emax) : kNBCta;
-      const bool inb = (j < T_n) && (bb == bmin);
-      if (j < T_n) flag[j] = (bb < bmin) ? 1 : 0;
+      const bool inb = (j < T_n) && (static_cast<int>(ebin[j]) == bmin);
       const unsigned int bal = __ballot_sync(0xffffffffu, inb);
+      if (bal == 0u) continue;
       int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(&s_info[1], __popc(bal));
+      if (lane == 0) base = atomicAdd(&s_info[1], __popc(bal));
       base = __shfl_sync(0xffffffffu, base, 0);
       const int pos = base + __popc(bal & ((1u << lane) - 1u));
-      if (inb && pos < kListCap) list[pos] = k;
+      if (inb && pos < kListCap) list[pos] = ukey[j];
     }
     __syncthreads();
     int m = s_info[1];
@@ -776,7 +785,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
         const int t = t0 + lane;
         const uint64_t k = (t < m) ? la[t] : 0ull;
         const int d = 255 - static_cast<int>((k >> shift) & 255u);
-        if (t < m) flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (d < b2) ? 1 : 0;
+        if (t < m && d < b2) keep_bit(kIdxMask - static_cast<int>(k & kIdxMask));
         const bool inb = (t < m) && (d == b2);
         const unsigned int bal = __ballot_sync(0xffffffffu, inb);
         int pos = 0;
@@ -803,8 +812,8 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
         const unsigned long long y = __shfl_up_sync(0xffffffffu, qv, o);
         if (lane >= o) qv += y;
       }
-      if (lane < m)
-        flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (static_cast<double>(above + qv) <= thr) ? 1 : 0;
+      if (lane < m && static_cast<double>(above + qv) <= thr)
+        keep_bit(kIdxMask - static_cast<int>(k & kIdxMask));
     } else if (wid == 0 && bmin < kNBCta) {
       const unsigned long long carry0 = above;
       uint64_t* lst = la;
@@ -816,7 +825,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
         for (int j0 = 0; j0 < T_n; j0 += 32) {
           const int j = j0 + lane;
           const uint64_t k = (j < T_n) ? ukey[j] : 0ull;
-          const bool inb = (j < T_n) && (bin_of<kNBCta>(k, emax) == bmin);
+          const bool inb = (j < T_n) && (static_cast<int>(ebin[j]) == bmin);
           const unsigned int bal = __ballot_sync(0xffffffffu, inb);
           __syncwarp();
           if (inb) lst[mm + __popc(bal & ((1u << lane) - 1u))] = k;
@@ -841,11 +850,11 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
           if (lane >= o) qv += y;
         }
         const unsigned long long c = carry + qv;
-        if (t < m) flag[kIdxMask - static_cast<int>(k & kIdxMask)] = (static_cast<double>(c) <= thr) ? 1 : 0;
+        if (t < m && static_cast<double>(c) <= thr) keep_bit(kIdxMask - static_cast<int>(k & kIdxMask));
         carry = __shfl_sync(0xffffffffu, c, 31);
       }
     }
-    if (tid == 0) flag[kIdxMask - static_cast<int>(kmax & kIdxMask)] = 1;   // guard
+    if (tid == 0) keep_bit(kIdxMask - static_cast<int>(kmax & kIdxMask));   // guard
   }
   __syncthreads();
 
@@ -858,7 +867,7 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   const int ch = ((T_n + kCtaWarps - 1) / kCtaWarps + 31) / 32 * 32;
   const int c0 = wid * ch, c1 = min(T_n, c0 + ch);
   auto kept = [&](int j) {
-    bool f = flagged ? true : (flag[j] != 0);
+    bool f = flagged || static_cast<int>(ebin[j]) < bmin || ((dec[j >> 5] >> (j & 31)) & 1u);
     if (row_fix || ((forced[j >> 5] >> (j & 31)) & 1u)) f = true;
     if (causal) {
       if (j >= n_live) f = false;
