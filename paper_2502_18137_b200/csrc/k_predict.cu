@@ -38,12 +38,19 @@ namespace {
 // share an SM -- v1 staged all of d at once, 135 KB, one CTA per SM, and the
 // SM idled during every load: 25 % occupancy, ncu r02_pred128k); 8 warps,
 // each a 16-row x 32-key register tile (2 x 4 DMMA fragments per k-step:
-// 6 fragment loads per 8 DMMAs).
-constexpr int kTile = 64;          // query blocks x key blocks per CTA
+// 6 fragment loads per 8 DMMAs).  SPARGE_SHAT_TN (A/B knob) widens or
+// narrows the CTA's key tile: 128 (2 CTAs/SM) and 32 (4 CTAs/SM) measured
+// 4 % / 2 % slower at 128K (profiles/r02/r02_s8_shat_tile_ab.txt).
+#ifndef SPARGE_SHAT_TN
+#define SPARGE_SHAT_TN 64
+#endif
+constexpr int kTile = 64;          // query blocks per CTA
+constexpr int kTileN = SPARGE_SHAT_TN;   // key blocks per CTA
+constexpr int kFragN = kTileN / 16;      // 8-key fragments per warp (two key halves)
 constexpr int kKC = 32;            // d chunk (doubles) per stage
 constexpr int kKR = kKC + 4;       // padded chunk row: kKR % 16 == 4 (conflict-free fragments)
 constexpr int kGemmThreads = 256;
-constexpr size_t kGemmSmem = sizeof(double) * 2 /*stages*/ * 2 /*Q, K*/ * kTile * kKR;
+constexpr size_t kGemmSmem = sizeof(double) * 2 /*stages*/ * (kTile + kTileN) * kKR;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
@@ -62,8 +69,8 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
             double* __restrict__ shat) {
   constexpr int NCH = D / kKC;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* stage = reinterpret_cast<double*>(smem);       // [2][2][kTile][kKR]
-  const int j0 = blockIdx.x * kTile, i0 = blockIdx.y * kTile, bhq = blockIdx.z;
+  double* stage = reinterpret_cast<double*>(smem);       // [2][kTile + kTileN][kKR]
+  const int j0 = blockIdx.x * kTileN, i0 = blockIdx.y * kTile, bhq = blockIdx.z;
   // causal: a tile whose every key block is dead for every query block of
   // the tile (R8-i) is never read by k_topcdf_rows -- skip it
   if (causal && j0 * bk > min((min(i0 + kTile, T_m)) * bq, N) - 1) return;
@@ -75,12 +82,12 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
 
   // chunk c of 64 pooled-Q rows and 64 pooled-K rows (zero beyond T_m / T_n)
   auto issue = [&](int c, int buf) {
-    double* sq = stage + (buf * 2 + 0) * kTile * kKR;
-    double* sk = stage + (buf * 2 + 1) * kTile * kKR;
+    double* sq = stage + buf * (kTile + kTileN) * kKR;
+    double* sk = sq + kTile * kKR;
     constexpr int CH = kKC / 2;      // 16-B pieces per chunk row
-    for (int e = tid; e < 2 * kTile * CH; e += kGemmThreads) {
-      const int which = e / (kTile * CH);
-      const int rr = (e / CH) % kTile, cc = e % CH;
+    for (int e = tid; e < (kTile + kTileN) * CH; e += kGemmThreads) {
+      const int which = e >= kTile * CH;
+      const int rr = which ? e / CH - kTile : e / CH, cc = e % CH;
       double* dst = (which ? sk : sq) + rr * kKR + 2 * cc;
       const bool ok = which ? (j0 + rr < T_n) : (i0 + rr < T_m);
       if (ok) {
@@ -100,11 +107,11 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
   // k = lane%4; B k = lane%4, n = lane/4; C row = lane/4, cols 2*(lane%4)+{0,1}
   const int rs = wid & 3, kh = wid >> 2;
   const int g = lane >> 2, t4 = lane & 3;
-  double acc[2][4][2];
+  double acc[2][kFragN][2];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int kt = 0; kt < 4; ++kt) acc[r][kt][0] = acc[r][kt][1] = 0.0;
+    for (int kt = 0; kt < kFragN; ++kt) acc[r][kt][0] = acc[r][kt][1] = 0.0;
 
   issue(0, 0);
   for (int c = 0; c < NCH; ++c) {
@@ -115,15 +122,15 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    const double* sq = stage + ((c & 1) * 2 + 0) * kTile * kKR;
-    const double* sk = stage + ((c & 1) * 2 + 1) * kTile * kKR;
+    const double* sq = stage + (c & 1) * (kTile + kTileN) * kKR;
+    const double* sk = sq + kTile * kKR;
     const double* a0 = sq + (16 * rs + g) * kKR + t4;
-    const double* b0 = sk + (32 * kh + g) * kKR + t4;
+    const double* b0 = sk + (8 * kFragN * kh + g) * kKR + t4;
 #pragma unroll
     for (int ks = 0; ks < kKC / 4; ++ks) {
       const double a_lo = a0[4 * ks], a_hi = a0[8 * kKR + 4 * ks];
 #pragma unroll
-      for (int kt = 0; kt < 4; ++kt) {
+      for (int kt = 0; kt < kFragN; ++kt) {
         const double bv = b0[8 * kt * kKR + 4 * ks];
         dmma_884(acc[0][kt][0], acc[0][kt][1], a_lo, bv);
         dmma_884(acc[1][kt][0], acc[1][kt][1], a_hi, bv);
@@ -138,8 +145,8 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
     if (row >= T_m) continue;
     double* out = shat + (qbase + row) * T_n;
 #pragma unroll
-    for (int kt = 0; kt < 4; ++kt) {
-      const int key = j0 + 32 * kh + 8 * kt + 2 * t4;
+    for (int kt = 0; kt < kFragN; ++kt) {
+      const int key = j0 + 8 * kFragN * kh + 8 * kt + 2 * t4;
       if (key < T_n) out[key] = acc[r][kt][0] * inv_sqrt_d;
       if (key + 1 < T_n) out[key + 1] = acc[r][kt][1] * inv_sqrt_d;
     }
@@ -914,7 +921,7 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
   cudaError_t e = cudaFuncSetAttribute(k_shat_dmma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem_g));
   if (e != cudaSuccess) return e;
-  dim3 g1((T_n + kTile - 1) / kTile, (T_m + kTile - 1) / kTile, s.B * s.Hq);
+  dim3 g1((T_n + kTileN - 1) / kTileN, (T_m + kTile - 1) / kTile, s.B * s.Hq);
   k_shat_dmma<D><<<g1, kGemmThreads, smem_g, stream>>>(q_pooled, k_pooled, s.Hq, s.Hkv, T_m, T_n,
                                                         s.N, s.bq, s.bk, s.causal, shat);
   const int rows = s.B * s.Hq * T_m;
