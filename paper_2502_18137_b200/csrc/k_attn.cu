@@ -334,12 +334,6 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   // barrier / TMEM address derived from it) as warp-uniform
   const int warp = __shfl_sync(0xffffffffu, warp_id(), 0), lane = lane_id();
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
-  // this CTA's work item from the launch order of k_order (the items with
-  // the most kept blocks launch first)
-  const int item = __ldg(p.order + blockIdx.x);
-  const int bhq = item / p.T_m, i = item - bhq * p.T_m;
-  const int b = bhq / p.Hq, hq = bhq % p.Hq;
-  const int bkv = b * p.Hkv + hq / p.group;
 
   int8_t* sQ = reinterpret_cast<int8_t*>(smem + L::OFF_Q);
   int8_t* sK = reinterpret_cast<int8_t*>(smem + L::OFF_K);
@@ -382,6 +376,16 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  // PDL (sparge_internal.h): the set-up above (barriers, bias operands, TMEM)
+  // overlapped the previous kernel's tail; its outputs are visible from here
+  griddep_wait();
+  griddep_launch();
+  // this CTA's work item from the launch order of k_order (the items with
+  // the most kept blocks launch first)
+  const int item = __ldg(p.order + blockIdx.x);
+  const int bhq = item / p.T_m, i = item - bhq * p.T_m;
+  const int b = bhq / p.Hq, hq = bhq % p.Hq;
+  const int bkv = b * p.Hkv + hq / p.group;
 
   const int64_t row_id = static_cast<int64_t>(bhq) * p.T_m + i;
   const int n_tiles = p.cnt[row_id];
@@ -775,8 +779,7 @@ cudaError_t launch_t(const CUtensorMap& mq, const CUtensorMap& mk, const CUtenso
   const int smem = Smem<D, QK16, PV8>::BYTES + 1024;   // + slack for 1024-B alignment
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(p.T_m * B * p.Hq), THREADS, smem, stream>>>(mq, mk, mv, p);
-  return cudaGetLastError();
+  return launch_k(kPdlAttn, kern, dim3(p.T_m * B * p.Hq), dim3(THREADS), smem, stream, mq, mk, mv, p);
 }
 
 

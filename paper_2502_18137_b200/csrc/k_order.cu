@@ -22,6 +22,7 @@
 // independent and writes its own rows).
 #include <cstdint>
 
+#include "sm100.cuh"
 #include "sparge_internal.h"
 
 namespace sparge {
@@ -83,6 +84,8 @@ k_order_head(const int32_t* __restrict__ cnt, int n, int tn, int per_group, int 
   __shared__ int warp_sum[kThreads / 32];
   __shared__ int s_cut;
   const int tid = threadIdx.x;
+  griddep_wait();      // PDL (sparge_internal.h)
+  griddep_launch();
   for (int b = tid; b <= tn; b += kThreads) h[b] = 0;
   for (int g = tid; g < n_groups; g += kThreads) gcount[g] = 0;
   __syncthreads();
@@ -126,6 +129,13 @@ k_order_groups(const int32_t* __restrict__ cnt, int n_all, int tn, int per_group
   extern __shared__ int h[];      // tn + 1 bucket counts, then write offsets
   __shared__ int warp_sum[kThreads / 32];
   const int tid = threadIdx.x;
+  // PDL: trigger BEFORE waiting -- the next kernel (the V stage, which needs
+  // nothing from k_order and waits for this grid at its end, or the
+  // attention kernel, which waits at its start) may start right away;
+  // k_order_head ran its wait before triggering this launch, so everything
+  // before the attention call is complete by now
+  griddep_launch();
+  griddep_wait();
   const int cut = meta[0];
   const int base = static_cast<int>(blockIdx.x) * per_group;
   const int n = min(per_group, n_all - base);
@@ -162,9 +172,11 @@ cudaError_t launch_order(const int32_t* cnt, int n, int tn, int per_group, int n
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_order_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_groups);
   if (e != cudaSuccess) return e;
-  k_order_head<<<1, kThreads, smem_head, stream>>>(cnt, n, tn, per_group, n_groups, n_long, order, meta);
-  k_order_groups<<<n_groups, kThreads, smem_groups, stream>>>(cnt, n, tn, per_group, order, meta);
-  return cudaGetLastError();
+  e = launch_k(kPdlOrder, k_order_head, dim3(1), dim3(kThreads), smem_head, stream, cnt, n, tn, per_group,
+               n_groups, n_long, order, meta);
+  if (e != cudaSuccess) return e;
+  return launch_k(kPdlOrder, k_order_groups, dim3(n_groups), dim3(kThreads), smem_groups, stream, cnt, n, tn,
+                  per_group, order, static_cast<const int32_t*>(meta));
 }
 
 }  // namespace sparge

@@ -15,7 +15,10 @@
 //               cores (mma.sync m8n8k4 f64, DMMA): 64 query blocks x 64 key
 //               blocks per CTA staged in shared memory (rows padded to d+4
 //               doubles: the A/B fragment loads are bank-conflict free), one
-//               8-row strip per warp; written to the workspace.
+//               8-row strip per warp; written to the workspace with -inf in
+//               the fixed K columns (s_kj < theta), so the TopCdf kernels
+//               bulk-copy a row into shared memory and read the forced
+//               columns back from it (no per-row k_sim reads).
 // k_topcdf_rows one warp per (head, query block): masks, softmax, the
 //               sort-free binned TopCdf selection (topcdf_binned: fixed-point
 //               integer bin masses, only the boundary bin sorted), forcing,
@@ -25,6 +28,7 @@
 #include <cstdlib>
 #include <cfloat>
 
+#include "sm100.cuh"
 #include "sparge_internal.h"
 
 namespace sparge {
@@ -65,6 +69,7 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 template <int D>
 __global__ void __launch_bounds__(kGemmThreads)
 k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_pooled,
+            const double* __restrict__ k_sim, double theta,
             int Hq, int Hkv, int T_m, int T_n, int N, int bq, int bk, int causal,
             double* __restrict__ shat) {
   constexpr int NCH = D / kKC;
@@ -74,6 +79,8 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
   // causal: a tile whose every key block is dead for every query block of
   // the tile (R8-i) is never read by k_topcdf_rows -- skip it
   if (causal && j0 * bk > min((min(i0 + kTile, T_m)) * bq, N) - 1) return;
+  griddep_wait();      // PDL (sparge_internal.h)
+  griddep_launch();
   const int hq = bhq % Hq, b = bhq / Hq;
   const int hkv = hq / (Hq / Hkv);
   const int64_t qbase = static_cast<int64_t>(bhq) * T_m;
@@ -138,7 +145,20 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
     }
     __syncthreads();          // the buffer is refilled two chunks later
   }
+  // epilogue: S^ / sqrt(d), and -inf in the columns of the fixed K blocks
+  // (s_kj < theta, strict, R5) -- the TopCdf kernels read the forced
+  // columns back as the -inf entries of a live column (a finite q.k never is
+  // -inf), so they need not re-read k_sim for every row.  Pairs of keys as one
+  // 16-B store when the row offset is even (T_n even).
   const double inv_sqrt_d = 1.0 / sqrt(static_cast<double>(D));
+  bool fk[kFragN][2];
+#pragma unroll
+  for (int kt = 0; kt < kFragN; ++kt) {
+    const int key = j0 + 8 * kFragN * kh + 8 * kt + 2 * t4;
+    fk[kt][0] = key < T_n && __ldg(k_sim + kbase + key) < theta;
+    fk[kt][1] = key + 1 < T_n && __ldg(k_sim + kbase + key + 1) < theta;
+  }
+  const bool pair_ok = (T_n & 1) == 0;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const int row = i0 + 16 * rs + 8 * r + g;
@@ -147,8 +167,14 @@ k_shat_dmma(const double* __restrict__ q_pooled, const double* __restrict__ k_po
 #pragma unroll
     for (int kt = 0; kt < kFragN; ++kt) {
       const int key = j0 + 8 * kFragN * kh + 8 * kt + 2 * t4;
-      if (key < T_n) out[key] = acc[r][kt][0] * inv_sqrt_d;
-      if (key + 1 < T_n) out[key + 1] = acc[r][kt][1] * inv_sqrt_d;
+      const double v0 = fk[kt][0] ? -INFINITY : acc[r][kt][0] * inv_sqrt_d;
+      const double v1 = fk[kt][1] ? -INFINITY : acc[r][kt][1] * inv_sqrt_d;
+      if (pair_ok && key + 1 < T_n) {
+        *reinterpret_cast<double2*>(out + key) = make_double2(v0, v1);
+      } else {
+        if (key < T_n) out[key] = v0;
+        if (key + 1 < T_n) out[key + 1] = v1;
+      }
     }
   }
 }
@@ -478,13 +504,15 @@ __device__ void topcdf_binned(uint64_t* ukey, uint32_t* bins, uint8_t* flag, int
 template <int D>
 __global__ void __launch_bounds__(kMaxRowWarps * 32)
 k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
-              const double* __restrict__ k_sim, int Hq, int Hkv, int N, int T_m, int T_n,
+              int Hq, int Hkv, int N, int T_m, int T_n,
               int rows_total, int bq, int bk, int causal, double tau, double theta,
               uint8_t* __restrict__ mask, int32_t* __restrict__ lut, int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int row_warps = blockDim.x >> 5;
   const int row = blockIdx.x * row_warps + wid;          // (b*Hq + hq)*T_m + i
+  griddep_wait();      // PDL (sparge_internal.h)
+  griddep_launch();
   if (row >= rows_total) return;
   // per warp: T_n keys (8 B), T_n flags, kNB bin sums (8 B)
   const size_t per_warp = row_smem_bytes(T_n);
@@ -496,40 +524,41 @@ k_topcdf_rows(const double* __restrict__ shat, const double* __restrict__ q_sim,
   uint8_t* flag = base_w + nk * 8 + 16 * kNB;
   uint32_t* forced = reinterpret_cast<uint32_t*>(flag + ((T_n + 15) / 16) * 16);   // s_k < theta
 
-  const int i = row % T_m, bhq = row / T_m;
-  const int hq = bhq % Hq, b = bhq / Hq;
-  const int64_t kbase = (static_cast<int64_t>(b) * Hkv + hq / (Hq / Hkv)) * T_n;
+  const int i = row % T_m;
   const int last_q = min((i + 1) * bq, N) - 1;
   // causal: key blocks j >= n_live are dead for this row (R8-i) -- never
   // loaded (k_shat_dmma does not compute tiles that are dead for a whole CTA)
   const int n_live = causal ? min(T_n, last_q / bk + 1) : T_n;
   const double* srow = shat + static_cast<int64_t>(row) * T_n;
 
-  // ---- S^ row with the -inf columns (fixed K blocks, causally dead) ----
-  // the row's global loads batched kLoadBatch deep (the smem stores between
-  // them would otherwise serialise one load latency per 32 entries)
-  constexpr int kLoadBatch = 8;
-  double mx = -INFINITY;
-  for (int jb = 0; jb < T_n; jb += 32 * kLoadBatch) {     // warp-uniform bound (ballots below)
-    const int j0 = jb + lane;
-    double sv[kLoadBatch], kv[kLoadBatch];
-#pragma unroll
-    for (int u = 0; u < kLoadBatch; ++u) {
-      const int j = j0 + 32 * u;
-      sv[u] = (j < n_live) ? __ldg(srow + j) : -INFINITY;
-      kv[u] = (j < n_live) ? __ldg(k_sim + kbase + j) : 1.0;
+  // ---- S^ row (k_shat_dmma already wrote -inf in the fixed K columns) ----
+  // one bulk copy of the row's live entries into the key array (T_n even:
+  // 16-B aligned rows), completing on this warp's mbarrier; entries j >=
+  // n_live (causally dead, possibly never written) become -inf here.  A
+  // forced column is a live -inf entry.
+  __shared__ __align__(8) uint64_t s_bar[kMaxRowWarps];
+  const bool bulk = (T_n & 1) == 0;
+  if (bulk) {
+    if (lane == 0) {
+      mbar_init(s_bar + wid, 1);
+      fence_mbar_init();
+      const uint32_t bytes = static_cast<uint32_t>((n_live + 1) & ~1) * 8u;
+      mbar_arrive_expect_tx(s_bar + wid, bytes);
+      bulk_g2s(key, srow, bytes, s_bar + wid);
     }
-#pragma unroll
-    for (int u = 0; u < kLoadBatch; ++u) {
-      const int j = j0 + 32 * u;
-      const bool fc = (j < n_live) && (kv[u] < theta);
-      const unsigned int fb = __ballot_sync(0xffffffffu, fc);
-      if (lane == 0 && j - lane < T_n) forced[(j - lane) >> 5] = fb;
-      if (j < T_n) {
-        const double s = fc ? -INFINITY : sv[u];
-        key[j] = s;
-        mx = fmax(mx, s);
-      }
+    __syncwarp();
+    mbar_wait(s_bar + wid, 0);
+  }
+  double mx = -INFINITY;
+  for (int j0 = 0; j0 < T_n; j0 += 32) {                  // warp-uniform bound (ballots below)
+    const int j = j0 + lane;
+    double sv = -INFINITY;
+    if (j < n_live) sv = bulk ? key[j] : __ldg(srow + j);
+    const unsigned int fb = __ballot_sync(0xffffffffu, j < n_live && sv == -INFINITY);
+    if (lane == 0) forced[j0 >> 5] = fb;
+    if (j < T_n) {
+      if (!bulk || j >= n_live) key[j] = sv;
+      mx = fmax(mx, sv);
     }
   }
   mx = warp_max(mx);
@@ -621,7 +650,7 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 template <int D>
 __global__ void __launch_bounds__(kCtaThreads)
 k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
-             const double* __restrict__ k_sim, int Hq, int Hkv, int N, int T_m, int T_n,
+             int Hq, int Hkv, int N, int T_m, int T_n,
              int bq, int bk, int causal, double tau, double theta,
              uint8_t* __restrict__ mask, int32_t* __restrict__ lut, int32_t* __restrict__ cnt) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -632,6 +661,8 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   __shared__ int s_wcount[kCtaWarps];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int row = blockIdx.x;               // (b*Hq + hq)*T_m + i
+  griddep_wait();      // PDL (sparge_internal.h)
+  griddep_launch();
   uint64_t* ukey = reinterpret_cast<uint64_t*>(smem);
   double* key = reinterpret_cast<double*>(ukey);
   const size_t nk = static_cast<size_t>(pow2ceil(T_n));
@@ -647,40 +678,39 @@ k_topcdf_cta(const double* __restrict__ shat, const double* __restrict__ q_sim,
   uint32_t* dec = forced + forced_bytes(T_n) / 4;
   static_assert(kNBCta == 256, "bin indices stored as u8");
 
-  const int i = row % T_m, bhq = row / T_m;
-  const int hq = bhq % Hq, b = bhq / Hq;
-  const int64_t kbase = (static_cast<int64_t>(b) * Hkv + hq / (Hq / Hkv)) * T_n;
+  const int i = row % T_m;
   const int last_q = min((i + 1) * bq, N) - 1;
   const int n_live = causal ? min(T_n, last_q / bk + 1) : T_n;
   const double* srow = shat + static_cast<int64_t>(row) * T_n;
 
-  // ---- S^ row with the -inf columns (fixed K blocks, causally dead) ----
-  constexpr int kLoadBatch = 4;
-  double mx = -INFINITY;
-  for (int jb = 0; jb < T_n; jb += kCtaThreads * kLoadBatch) {   // uniform bound (ballots)
-    const int j0 = jb + tid;
-    double sv[kLoadBatch], kv[kLoadBatch];
-#pragma unroll
-    for (int u = 0; u < kLoadBatch; ++u) {
-      const int j = j0 + kCtaThreads * u;
-      sv[u] = (j < n_live) ? __ldg(srow + j) : -INFINITY;
-      kv[u] = (j < n_live) ? __ldg(k_sim + kbase + j) : 1.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kLoadBatch; ++u) {
-      const int j = j0 + kCtaThreads * u;
-      const bool fc = (j < n_live) && (kv[u] < theta);
-      const unsigned int fb = __ballot_sync(0xffffffffu, fc);
-      if (lane == 0 && j - lane < T_n) forced[(j - lane) >> 5] = fb;
-      if (j < T_n) {
-        const double sj = fc ? -INFINITY : sv[u];
-        key[j] = sj;
-        mx = fmax(mx, sj);
-      }
-    }
+  // ---- S^ row (k_shat_dmma already wrote -inf in the fixed K columns):
+  // one bulk copy of the live entries into the key array (T_n even), as in
+  // k_topcdf_rows; the bins are cleared while it lands ----
+  __shared__ __align__(8) uint64_t s_bar;
+  const bool bulk = (T_n & 1) == 0;
+  if (bulk && tid == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+    const uint32_t bytes = static_cast<uint32_t>((n_live + 1) & ~1) * 8u;
+    mbar_arrive_expect_tx(&s_bar, bytes);
+    bulk_g2s(key, srow, bytes, &s_bar);
   }
   for (int t = tid; t < 3 * kNBCta; t += kCtaThreads) bins[t] = 0u;
   for (int t = tid; t < static_cast<int>(forced_bytes(T_n) / 4); t += kCtaThreads) dec[t] = 0u;
+  __syncthreads();                           // s_bar initialised
+  if (bulk) mbar_wait(&s_bar, 0);
+  double mx = -INFINITY;
+  for (int j0 = 0; j0 < T_n; j0 += kCtaThreads) {   // uniform bound (ballots)
+    const int j = j0 + tid;
+    double sv = -INFINITY;
+    if (j < n_live) sv = bulk ? key[j] : __ldg(srow + j);
+    const unsigned int fb = __ballot_sync(0xffffffffu, j < n_live && sv == -INFINITY);
+    if (lane == 0 && j - lane < T_n) forced[(j - lane) >> 5] = fb;
+    if (j < T_n) {
+      if (!bulk || j >= n_live) key[j] = sv;
+      mx = fmax(mx, sv);
+    }
+  }
   mx = block_max(mx, red);
   const bool flagged = (mx == -INFINITY);   // every K block fixed / dead (R7)
   int bmin = kNBCta;                         // entries of bins < bmin are kept
@@ -922,10 +952,11 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
                                        static_cast<int>(smem_g));
   if (e != cudaSuccess) return e;
   dim3 g1((T_n + kTileN - 1) / kTileN, (T_m + kTile - 1) / kTile, s.B * s.Hq);
-  k_shat_dmma<D><<<g1, kGemmThreads, smem_g, stream>>>(q_pooled, k_pooled, s.Hq, s.Hkv, T_m, T_n,
-                                                        s.N, s.bq, s.bk, s.causal, shat);
   const int rows = s.B * s.Hq * T_m;
   const double tau_d = static_cast<double>(tau), theta_d = static_cast<double>(theta);
+  e = launch_k(kPdlPredict, k_shat_dmma<D>, g1, dim3(kGemmThreads), smem_g, stream, q_pooled, k_pooled, k_sim,
+               theta_d, s.Hq, s.Hkv, T_m, T_n, s.N, s.bq, s.bk, s.causal, shat);
+  if (e != cudaSuccess) return e;
   // long rows: one CTA of kCtaWarps warps per row (occupancy); short rows:
   // one warp per row, up to kMaxRowWarps rows per CTA
   if (T_n > cta_row_min_tn()) {
@@ -933,10 +964,9 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
     e = cudaFuncSetAttribute(k_topcdf_cta<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem_c));
     if (e != cudaSuccess) return e;
-    k_topcdf_cta<D><<<rows, kCtaThreads, smem_c, stream>>>(
-        shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, s.bq, s.bk, s.causal, tau_d, theta_d,
-        mask, lut, cnt);
-    return cudaGetLastError();
+    return launch_k(kPdlPredict, k_topcdf_cta<D>, dim3(rows), dim3(kCtaThreads), smem_c, stream, shat, q_sim,
+                    s.Hq, s.Hkv, s.N, T_m, T_n, s.bq, s.bk, s.causal, tau_d, theta_d, mask, lut,
+                    cnt);
   }
   // rows per CTA: up to kMaxRowWarps, as many as fit the shared memory
   const size_t per_warp = row_smem_bytes(T_n);
@@ -946,10 +976,9 @@ cudaError_t launch_d(const sparge_shape& s, const double* q_pooled, const double
   e = cudaFuncSetAttribute(k_topcdf_rows<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem_r));
   if (e != cudaSuccess) return e;
-  k_topcdf_rows<D><<<(rows + warps - 1) / warps, warps * 32, smem_r, stream>>>(
-      shat, q_sim, k_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, s.bq, s.bk, s.causal, tau_d, theta_d,
-      mask, lut, cnt);
-  return cudaGetLastError();
+  return launch_k(kPdlPredict, k_topcdf_rows<D>, dim3((rows + warps - 1) / warps), dim3(warps * 32), smem_r,
+                  stream, shat, q_sim, s.Hq, s.Hkv, s.N, T_m, T_n, rows, s.bq, s.bk, s.causal,
+                  tau_d, theta_d, mask, lut, cnt);
 }
 
 }  // namespace

@@ -9,6 +9,7 @@
 #include <cuda_fp16.h>
 #include <cstdint>
 
+#include "sm100.cuh"
 #include "sparge_internal.h"
 
 namespace sparge {
@@ -19,13 +20,21 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_vprep(const uint16_t* __restrict__ v, int64_t sb, int64_t sh, int64_t sn,
         const int32_t* __restrict__ perm, int Hkv, int N, int n_pad,
-        uint16_t* __restrict__ vt) {
+        uint16_t* __restrict__ vt, int early) {
   constexpr int BK = 64;
   constexpr int PAD = 8;
   __shared__ __align__(16) uint16_t tile[BK][D + PAD];
   const int jb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x;
   const uint16_t* vbh = v + b * sb + h * sh;
+  // PDL (sparge_internal.h).  early = 1 when launched right after k_order
+  // inside one attention call (sparge_attn_fwd): V and V^T are touched by no
+  // kernel after the caller's last one before the call (complete: k_order_head
+  // waited for it before k_order_groups let this grid start), so the staging
+  // overlaps the launch-order kernels and waits for them only at its end --
+  // the attention kernel's wait on this grid then covers k_order too
+  if (!early) griddep_wait();
+  griddep_launch();
   // load 64 rows x D (16 B per thread per step), gathered through perm; the
   // source rows are looked up first so their loads are all in flight at once
   constexpr int CPR = D / 8;
@@ -68,20 +77,18 @@ k_vprep(const uint16_t* __restrict__ v, int64_t sb, int64_t sh, int64_t sn,
     o4[0] = make_uint4(w[0], w[1], w[2], w[3]);
     o4[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
+  if (early) griddep_wait();   // this grid completes only after k_order has
 }
 
 }  // namespace
 
 cudaError_t launch_vprep(const sparge_shape& s, const void* v, sparge_strides st,
-                         const int32_t* perm, void* vt, int n_pad, cudaStream_t stream) {
+                         const int32_t* perm, void* vt, int n_pad, bool early,
+                         cudaStream_t stream) {
   dim3 grid(n_pad / 64, s.Hkv, s.B);
-  if (s.d == 128)
-    k_vprep<128><<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(v), st.b, st.h, st.n,
-                                           perm, s.Hkv, s.N, n_pad, static_cast<uint16_t*>(vt));
-  else
-    k_vprep<64><<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(v), st.b, st.h, st.n,
-                                          perm, s.Hkv, s.N, n_pad, static_cast<uint16_t*>(vt));
-  return cudaGetLastError();
+  return launch_k(kPdlVprep, s.d == 128 ? k_vprep<128> : k_vprep<64>, grid, dim3(256), 0, stream,
+                  static_cast<const uint16_t*>(v), st.b, st.h, st.n, perm, s.Hkv, s.N, n_pad,
+                  static_cast<uint16_t*>(vt), early ? 1 : 0);
 }
 
 }  // namespace sparge

@@ -240,10 +240,13 @@ int attn_fwd_impl(const sparge_shape* shape, const void* qq, const float* dq,
       ws + kStatusBytes + vt_bytes(shape) + (pv8 ? 2 * chan_bytes(shape) : 0));
 
   cudaError_t e = cudaSuccess;
-  if (!(flags & SPARGE_ATTN_SKIP_VPREP)) {
+  // the whole call (flags 0, 16-bit V): k_order first, then the V stage,
+  // which overlaps it (PDL, k_vprep.cu), then the attention kernel
+  const bool vprep_after_order = flags == 0u && !pv8;
+  if (!(flags & SPARGE_ATTN_SKIP_VPREP) && !vprep_after_order) {
     e = pv8 ? launch_vprep_fp8(s, v, v_str, perm, static_cast<uint8_t*>(vt), amax_bits, v_scale,
                                n_pad, st)
-            : launch_vprep(s, v, v_str, perm, vt, n_pad, st);
+            : launch_vprep(s, v, v_str, perm, vt, n_pad, false, st);
     if (e != cudaSuccess) return SPARGE_ECUDA;
   }
   if (flags & SPARGE_ATTN_VPREP_ONLY) return SPARGE_OK;
@@ -297,6 +300,10 @@ int attn_fwd_impl(const sparge_shape* shape, const void* qq, const float* dq,
   e = launch_order(cnt, n_it, (s.N + 63) / 64, static_cast<int>(std::min<int64_t>(per_group, n_it)),
                    n_long, order, order + round256(static_cast<size_t>(n_it) * 4) / 4, st);
   if (e != cudaSuccess) return SPARGE_ECUDA;
+  if (vprep_after_order) {
+    e = launch_vprep(s, v, v_str, perm, vt, n_pad, true, st);
+    if (e != cudaSuccess) return SPARGE_ECUDA;
+  }
   e = launch_attn(s, mq, mk, mv, dq, dk, lut, cnt, lambda, perm, o, o_str, counters, status,
                   pv8 ? v_scale : nullptr, order, mpv, st);
   return e == cudaSuccess ? SPARGE_OK : SPARGE_ECUDA;
@@ -345,3 +352,14 @@ int sparge_attn_status(void* workspace, void* stream) {
 }
 
 }  // extern "C"
+
+namespace sparge {
+// PDL on the hot-path launches (sparge_internal.h); SPARGE_PDL=0 disables
+bool pdl_enabled(unsigned site) {
+  static const unsigned v = [] {
+    const char* e = std::getenv("SPARGE_PDL");
+    return e ? static_cast<unsigned>(std::strtoul(e, nullptr, 0)) : kPdlDefault;
+  }();
+  return (v & site) != 0u;
+}
+}  // namespace sparge

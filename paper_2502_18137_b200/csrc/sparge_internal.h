@@ -4,10 +4,47 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <utility>
 
 #include "../../include/sparge.h"
 
 namespace sparge {
+
+// Programmatic dependent launch (PDL).  The hot-path kernels are launched
+// with programmatic stream serialisation and begin with griddep_wait()
+// (before their first global-memory access: the kernel before them in the
+// stream has then completed and its writes are visible) followed by
+// griddep_launch() (sm100.cuh), so the next kernel's launch and its CTAs'
+// shared-memory / TMEM / barrier set-up overlap this kernel's tail instead of
+// following it.  Stream order is unchanged: every kernel still waits for its
+// predecessor before touching memory.  SPARGE_PDL (A/B runs) is a bit mask
+// over the launch sites below (kPdl*); a cleared bit launches that kernel
+// plainly (griddepcontrol.wait is then a no-op).
+enum : unsigned {
+  kPdlQuantQ = 1u, kPdlQuantK = 2u, kPdlPredict = 4u, kPdlVprep = 8u, kPdlOrder = 16u,
+  kPdlAttn = 32u
+};
+// default: every site but the two quantiser launches -- with PDL on the K
+// launch (its CTAs queued behind the persistent Q grid) the quantisation
+// stage measured ~11 us slower on Flux / 8K, the other sites ~1 % faster
+// per step (profiles/r02/r02_s11_pdl_mask.txt)
+constexpr unsigned kPdlDefault = kPdlPredict | kPdlVprep | kPdlOrder | kPdlAttn;
+bool pdl_enabled(unsigned site);
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(unsigned site, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled(site) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // 16-bit V^T staging layout: tile-major [B, Hkv, N_pad/64, d, 64] (each
 // 64-key tile one contiguous 16 KB (d=128) block: contiguous writes in
@@ -36,8 +73,11 @@ cudaError_t launch_predict(const sparge_shape& s, const double* q_pooled, const 
                            cudaStream_t stream);
 size_t predict_workspace_bytes(const sparge_shape& s);
 
+// early: launched right after k_order within one attention call -- the
+// staging overlaps k_order and waits for it at its end (PDL, k_vprep.cu)
 cudaError_t launch_vprep(const sparge_shape& s, const void* v, sparge_strides st,
-                         const int32_t* perm, void* vt, int n_pad, cudaStream_t stream);
+                         const int32_t* perm, void* vt, int n_pad, bool early,
+                         cudaStream_t stream);
 // f4: per-channel amax of V (into amax_bits, zeroed here), then V^T in FP8
 // E4M3 (x * fl32(448/amax_c)) and the dequant scales s_c = fl32(amax_c/448).
 cudaError_t launch_vprep_fp8(const sparge_shape& s, const void* v, sparge_strides st,
