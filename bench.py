@@ -675,7 +675,9 @@ def run_ours(args):
             pipe = sparge.HostPipeline(1, prob.Hq, prob.Hkv, N, d, causal=cfg["causal"],
                                        dtype=prob.q.dtype,
                                        chunks=max(c_ for c_ in (1, 2, 3, 4, 6, 8)
-                                                  if prob.Hkv % c_ == 0), device=dev)
+                                                  if prob.Hkv % c_ == 0), device=dev,
+                                       tail_split={"0": False, "1": True}.get(
+                                           os.environ.get("SPARGE_E2E_TAIL_SPLIT", "")))
 
             def e2e_step():
                 pipe(qh, kh, vh, oh, cfg["tau"], cfg["theta"], cfg["lam"], perm=prob.perm)

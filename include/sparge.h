@@ -12,7 +12,14 @@
  *     device memory, never synchronises the stream (except
  *     sparge_attn_status, which says so) and never prints.
  *   - All work is enqueued asynchronously on `stream` (a cudaStream_t passed
- *     as an opaque pointer; NULL = the legacy default stream).
+ *     as an opaque pointer; NULL = the legacy default stream).  Stream order
+ *     holds as for plain launches: the prediction, V-stage, launch-order and
+ *     attention kernels are launched with programmatic dependent launch
+ *     (CUDA PDL) and each waits (griddepcontrol.wait) for the work before it
+ *     in the stream to complete before it reads or writes global memory;
+ *     only their launch and on-chip set-up overlap the predecessor's tail.
+ *     A caller kernel that itself uses PDL must not trigger its dependents
+ *     before its outputs are written (the standard PDL contract).
  *   - Tensors of tokens are [B, H, N, d] with d contiguous; `sparge_strides`
  *     gives the element strides of the b, h and n axes.  Row starts must be
  *     16-byte aligned (d in {64, 128}, so stride_n*2 % 16 == 0).
@@ -243,7 +250,9 @@ int sparge_attn_fwd(const sparge_shape* shape,
                     void* workspace, size_t ws_bytes, void* stream);
 
 /* sparge_attn_fwd split into its two launches, for per-kernel timing:
- *   flags = 0                          same as sparge_attn_fwd
+ *   flags = 0                          same as sparge_attn_fwd (the launch
+ *                                      order kernels, then the V staging,
+ *                                      which overlaps them, then attention)
  *   flags = SPARGE_ATTN_VPREP_ONLY     only stage V^T (+ Hilbert gather) into
  *                                      the workspace
  *   flags = SPARGE_ATTN_SKIP_VPREP     only the attention kernel; V^T must

@@ -341,33 +341,76 @@ def sparge_forward(q, k, v, tau, theta, lam, causal=False, perm=None, buffers=No
     return o, bf
 
 
+def pipeline_plan(Hq, Hkv, chunks, tail_split=True):
+    """Chunks of q-heads for HostPipeline: [(q0, q1, k0, k1, copy_kv)], q-heads
+    [q0, q1) against kv-heads [k0, k1); copy_kv = this chunk brings K/V of
+    [k0, k1) to the device (the first chunk that reads them).  `chunks` equal
+    runs of whole kv-groups; with tail_split the last run is split so the
+    step's tail -- the last chunk's compute and its O copy, which nothing
+    overlaps -- is one q-head (or one MHA head): its kv-groups but the last
+    become one chunk, the last group's q-heads pieces of halving size
+    (group 4 -> 2, 1, 1).  Every chunk is whole kv-groups or lies inside one,
+    so each is an independent (B, q-heads, kv-heads) problem."""
+    group = Hq // Hkv
+    if Hkv % chunks:
+        chunks = 1
+    kv_per = Hkv // chunks
+    plan = [(c * kv_per * group, (c + 1) * kv_per * group, c * kv_per, (c + 1) * kv_per, True)
+            for c in range(chunks)]
+    if not tail_split:
+        return plan
+    q0, _, k0, k1, _ = plan.pop()
+    if k1 - k0 > 1:                                   # whole groups but the last
+        plan.append((q0, q0 + (k1 - 1 - k0) * group, k0, k1 - 1, True))
+    g0 = (k1 - 1) * group                             # the last group's q-heads
+    left, first = group, True
+    while left > 0:
+        n = max(1, left // 2) if left > 1 else 1
+        if left == 2:
+            n = 1
+        plan.append((g0, g0 + n, k1 - 1, k1, first))
+        g0, left, first = g0 + n, left - n, False
+    return plan
+
+
 class HostPipeline:
     """End-to-end SpargeAttn from pinned HOST buffers with copy/compute overlap.
 
     The (batch, kv-head group) problems are independent, so
-    the work is split into `chunks` groups of kv-heads: chunk c's host->device
-    copy runs on one stream, its five kernels (quantise Q, K; predict; V
-    stage; attention) on a second, and its O device->host copy on a third,
-    overlapping with the neighbouring chunks.  Device buffers are allocated
-    once.  All compute is the C-ABI kernels; this class only orchestrates
-    copies and streams (torch)."""
+    the work is split into chunks of heads (pipeline_plan): chunk c's
+    host->device copy runs on one stream, its kernels (quantise Q, K; predict;
+    k_order + V stage; attention) on a second, and its O device->host copy on
+    a third, overlapping with the neighbouring chunks; the last chunk is small
+    (tail_split) because its compute and O copy follow the last input byte.
+    Device buffers are allocated once.  All compute is the C-ABI kernels; this
+    class only orchestrates copies and streams (torch)."""
 
     def __init__(self, B, Hq, Hkv, N, d, causal=False, dtype=torch.bfloat16, chunks=4,
-                 device="cuda", sim_mode=SPARGE_SIM_COSINE, qk_dtype=SPARGE_QK_INT8):
-        if Hkv % chunks:
-            chunks = 1
+                 device="cuda", sim_mode=SPARGE_SIM_COSINE, qk_dtype=SPARGE_QK_INT8,
+                 tail_split=None):
         self.B, self.Hq, self.Hkv, self.N, self.d = B, Hq, Hkv, N, d
-        self.group = Hq // Hkv
-        self.chunks = chunks
-        self.kv_per = Hkv // chunks
-        self.q_per = self.kv_per * self.group
-        self.shape = make_shape(B, self.q_per, self.kv_per, N, d, causal, dtype, sim_mode, qk_dtype)
+        if tail_split is None:
+            # split the tail when a chunk's Q is large enough that its compute
+            # and O copy outweigh the extra chunks' fixed costs (measured,
+            # profiles/r02/r02_s14_e2e_tail_split.txt: Llama 32K -1.2 %,
+            # Mochi -4.6 %, CogVideoX -1.8 %, Flux 4.6K +5 %)
+            per = Hq // max(1, chunks if Hkv % max(1, chunks) == 0 else 1)
+            tail_split = B * per * N * d * 2 >= (8 << 20)
+        self.plan = pipeline_plan(Hq, Hkv, chunks, tail_split)
+        self.chunks = len(self.plan)
+        self.shapes, self.bufs = [], {}
+        for q0, q1, k0, k1, _ in self.plan:
+            sh = make_shape(B, q1 - q0, k1 - k0, N, d, causal, dtype, sim_mode, qk_dtype)
+            key = (q1 - q0, k1 - k0)
+            if key not in self.bufs:
+                self.bufs[key] = Buffers(sh, device=device, with_mask=False)
+            self.shapes.append(sh)
+        self.causal, self.qk_dtype = causal, qk_dtype
         kw = dict(device=device, dtype=dtype)
         self.q = torch.empty(B, Hq, N, d, **kw)
         self.k = torch.empty(B, Hkv, N, d, **kw)
         self.v = torch.empty(B, Hkv, N, d, **kw)
         self.o = torch.empty(B, Hq, N, d, **kw)
-        self.bufs = [Buffers(self.shape, device=device, with_mask=False) for _ in range(min(chunks, 2))]
         self.s_h2d = torch.cuda.Stream(device)
         self.s_comp = torch.cuda.Stream(device)
         self.s_d2h = torch.cuda.Stream(device)
@@ -379,23 +422,22 @@ class HostPipeline:
         cur = torch.cuda.current_stream()
         for s in (self.s_h2d, self.s_comp, self.s_d2h):
             s.wait_stream(cur)
-        done_prev_comp = None
-        for c in range(self.chunks):
-            qs = slice(c * self.q_per, (c + 1) * self.q_per)
-            ks = slice(c * self.kv_per, (c + 1) * self.kv_per)
+        for (q0, q1, k0, k1, copy_kv), sh in zip(self.plan, self.shapes):
+            qs, ks = slice(q0, q1), slice(k0, k1)
             with torch.cuda.stream(self.s_h2d):
+                if copy_kv:
+                    self.k[:, ks].copy_(kh[:, ks], non_blocking=True)
+                    self.v[:, ks].copy_(vh[:, ks], non_blocking=True)
                 self.q[:, qs].copy_(qh[:, qs], non_blocking=True)
-                self.k[:, ks].copy_(kh[:, ks], non_blocking=True)
-                self.v[:, ks].copy_(vh[:, ks], non_blocking=True)
                 ev_in = torch.cuda.Event()
                 ev_in.record(self.s_h2d)
-            bf = self.bufs[c % len(self.bufs)]
+            bf = self.bufs[(q1 - q0, k1 - k0)]
             with torch.cuda.stream(self.s_comp):
                 self.s_comp.wait_event(ev_in)
                 sparge_forward(self.q[:, qs], self.k[:, ks], self.v[:, ks], tau, theta, lam,
-                               causal=bool(self.shape.causal), perm=perm, buffers=bf,
+                               causal=bool(self.causal), perm=perm, buffers=bf,
                                out=self.o[:, qs], stream=self.s_comp,
-                               qk_dtype=self.shape.qk_dtype, counters=False)
+                               qk_dtype=self.qk_dtype, counters=False)
                 ev_out = torch.cuda.Event()
                 ev_out.record(self.s_comp)
             with torch.cuda.stream(self.s_d2h):

@@ -115,3 +115,31 @@ def test_predict_rejects_rows_longer_than_max_tn(sp):
         rc = sp._lib.sparge_predict_mask(ctypes.byref(shape), fake, fake, fake, fake, 0.9, 0.5,
                                          None, fake, fake, fake, ws, None)
         assert rc == sp.SPARGE_EINVAL
+
+
+@pytest.mark.parametrize("Hq,Hkv,chunks", [(32, 8, 8), (32, 8, 1), (24, 24, 8), (30, 30, 6),
+                                           (8, 4, 2), (4, 4, 4), (2, 1, 1), (1, 1, 1), (12, 4, 3)])
+def test_pipeline_plan_partitions_heads(sp, Hq, Hkv, chunks):
+    """HostPipeline's chunk plan (host logic only): the chunks partition the
+    q-heads in order; each chunk is whole kv-groups or lies inside one group
+    and is paired with exactly its kv-heads (GQA h -> h // group); every
+    kv-head is copied once, by the first chunk that reads it; with the tail
+    split the last chunk is one q-head."""
+    group = Hq // Hkv
+    for tail in (False, True):
+        plan = sp.pipeline_plan(Hq, Hkv, chunks, tail)
+        assert plan[0][0] == 0 and plan[-1][1] == Hq
+        copied = set()
+        for (q0, q1, k0, k1, copy_kv), nxt in zip(plan, plan[1:] + [None]):
+            assert q0 < q1 and (nxt is None or nxt[0] == q1)
+            assert k0 == q0 // group and k1 == (q1 - 1) // group + 1
+            whole = q0 % group == 0 and q1 % group == 0
+            assert whole or k1 - k0 == 1
+            if copy_kv:
+                assert not (set(range(k0, k1)) & copied)
+                copied |= set(range(k0, k1))
+            else:
+                assert set(range(k0, k1)) <= copied
+        assert copied == set(range(Hkv))
+        if tail:
+            assert plan[-1][1] - plan[-1][0] == 1
