@@ -30,5 +30,6 @@ t0 = orig(enable_timing=True); t0.record()
 run(); torch.cuda.synchronize()
 torch.cuda.Event = orig
 # pipeline records ev_in (after H2D) and ev_out (after compute) per chunk
-for c in range(chunks):
-    print(f"chunk {c}: H2D done {t0.elapsed_time(tl[2 * c]):7.3f}  compute done {t0.elapsed_time(tl[2 * c + 1]):7.3f}")
+for c, pl in enumerate(pipe.plan):
+    print(f"chunk {c} q-heads {pl[0]}-{pl[1] - 1}{' +K/V' if pl[4] else ''}: H2D done {t0.elapsed_time(tl[2 * c]):7.3f}  "
+          f"compute done {t0.elapsed_time(tl[2 * c + 1]):7.3f}")
