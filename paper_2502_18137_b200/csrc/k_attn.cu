@@ -107,8 +107,36 @@ constexpr int kPolyEvery64 = SPARGE_POLY_EVERY64;
 // warp 4, MMA issuer warp 5.  (Experiments with two query tiles per CTA, a
 // speculative exp pass and timing ablations live in the git history and
 // profiles/experiments/; DESIGN.md §6 has their measurements.)
+//
+// SPARGE_ATTN_8W=1 (round 2 option, off by default): two idle warps pad the CTA to 8 warps =
+// two warpgroups, launched at 128 registers per thread; the softmax
+// warpgroup raises its budget to kRegSoftmax and the producer / MMA / idle
+// warpgroup lowers its to kRegOther with setmaxnreg.  Why: with 6 warps at
+// ~160 registers a CTA puts 2 warps on two SM sub-partitions and 1 on the
+// other two, so a second CTA fits only in the complementary placement --
+// per-CTA timelines (scripts/cta_timeline.py) showed an SM whose YOUNGER CTA
+// exited first was never refilled until the older one exited too (Mochi 22K:
+// ~85 % of SMs at one CTA for 135 us, 12 % of slot time idle).  With 8 warps
+// every CTA puts exactly two warps (one per warpgroup) on each sub-partition
+// and fits next to any other.  Measured (profiles/r02/r02_s19_attn_8w.txt):
+// the refill gaps vanish (Mochi 22K 80 -> 10 us per slot: step -3.7 %) but
+// a tile costs ~2 % more (786 -> 805 ns/tile on Llama), so Llama, CogVideoX,
+// Flux and the sweep are 1-2 % slower -- not the default.  (A 6-warp CTA
+// cannot use setmaxnreg: it needs whole warpgroups; that variant hung.)
+#ifndef SPARGE_ATTN_8W
+#define SPARGE_ATTN_8W 0
+#endif
+constexpr bool kPad8 = SPARGE_ATTN_8W == 1;
+constexpr int kMaxSms = 256;
+__device__ unsigned g_sm_slots[kMaxSms];     // per-SM CTA-slot bits (kPad8)
 constexpr int WARP_LOAD = NSOFT, WARP_MMA = NSOFT + 1;
-constexpr int THREADS = (NSOFT + 2) * 32;
+constexpr int THREADS = (kPad8 ? 2 * NSOFT : NSOFT + 2) * 32;
+#ifndef SPARGE_REG_SOFTMAX
+#define SPARGE_REG_SOFTMAX 168
+#endif
+constexpr int kRegSoftmax = SPARGE_REG_SOFTMAX;      // setmaxnreg budgets: (softmax + other) / 2
+constexpr int kRegOther = 256 - SPARGE_REG_SOFTMAX;  // = 128 registers per warp pair
+static_assert(!kPad8 || (kRegSoftmax + kRegOther) / 2 * THREADS * 2 <= 65536, "two CTAs per SM");
 
 // Shared-memory plan of a CTA.  QK16 = the unquantised f1 kernel (16-bit Q,
 // K tiles stored as d/64 SWIZZLE_128B K-atoms of 128 B rows); with d = 128
@@ -334,6 +362,25 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   // barrier / TMEM address derived from it) as warp-uniform
   const int warp = __shfl_sync(0xffffffffu, warp_id(), 0), lane = lane_id();
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  // kPad8: which of its SM's two CTA slots this CTA holds (a per-SM bit mask
+  // in global memory, claimed here and released at exit).  Slot 0 runs the
+  // producer / MMA roles on warps 4 / 5 (sub-partitions 0 / 1), slot 1 on
+  // warps 6 / 7 (2 / 3), so two co-resident CTAs split the single-thread
+  // tcgen05 / TMA issue over the four sub-partitions.  A mask left stale by
+  // an aborted launch only costs balance: both bits taken -> slot 0.
+  // OFF_MISC + 4: the slot (0/1); + 8: the claimed bit (-1: none); + 12: smid
+  int* slot_smem = reinterpret_cast<int*>(smem + L::OFF_MISC + 4);
+  if (kPad8 && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned* w = g_sm_slots + (smid & (kMaxSms - 1));
+    int my_bit = -1;
+    if (!(atomicOr(w, 1u) & 1u)) my_bit = 0;
+    else if (!(atomicOr(w, 2u) & 2u)) my_bit = 1;
+    slot_smem[0] = my_bit > 0 ? 1 : 0;
+    slot_smem[1] = my_bit;
+    slot_smem[2] = static_cast<int>(smid);
+  }
 
   int8_t* sQ = reinterpret_cast<int8_t*>(smem + L::OFF_Q);
   int8_t* sK = reinterpret_cast<int8_t*>(smem + L::OFF_K);
@@ -376,6 +423,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  const int slot2 = kPad8 ? 2 * *slot_smem : 0;
+  const int warp_load = WARP_LOAD + slot2, warp_mma = WARP_MMA + slot2;
   // PDL (sparge_internal.h): the set-up above (barriers, bias operands, TMEM)
   // overlapped the previous kernel's tail; its outputs are visible from here
   griddep_wait();
@@ -394,8 +443,14 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   // P~V(u) of the last NSB tiles, u >= n - NSB, completes o_tail[u - max(0,
   // n - NSB)] -- a barrier used once, so its parity-0 wait is unambiguous
   auto wait_tail = [&](int u) { mbar_wait(o_tail + (u - max(0, n_tiles - NSB)), 0); };
+  // register budgets per warpgroup (kPad8), set at the top of each role's
+  // branch so the compiler allocates each role's code under its own budget
+  auto regs_other = [] {
+    if constexpr (kPad8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegOther));
+  };
 
-  if (warp == WARP_LOAD) {
+  if (warp == warp_load) {
+    regs_other();
     // ============================ TMA producer ============================
     // (the whole warp runs the loop, one elected lane issues: see sm100.cuh)
     if (n_tiles > 0) {
@@ -440,7 +495,8 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
         else tma_load_3d_ew(sV + vs * L::V_BYTES, &tmV, v_full + vs, j * BK, 0, bkv);
       }
     }
-  } else if (warp == WARP_MMA) {
+  } else if (warp == warp_mma) {
+    regs_other();
     // ============================ MMA issuer ==============================
     // (the whole warp runs the loop, one elected lane issues: see sm100.cuh)
     if (n_tiles > 0) {
@@ -525,7 +581,10 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
       }
       if (p.counters && lane == 0) atomicAdd(p.counters + bhq * 3 + 2, issued);
     }
+  } else if (warp >= NSOFT) {
+    regs_other();               // kPad8: the two idle warps
   } else {
+    if constexpr (kPad8) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
     // ============================ softmax warps ===========================
     const int quad = warp & 3;                 // TMEM lane quadrant = gate group I_w
     const int r = quad * 32 + lane;            // row within the tile == TMEM lane
@@ -762,10 +821,16 @@ k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == WARP_MMA) {
+  if (warp == WARP_MMA) {     // the allocating warp (MMA or idle role)
     __syncwarp();
     tc_fence_after();
     tmem_dealloc<256>(tmem_base);
+  }
+  if (kPad8 && threadIdx.x == 0 && slot_smem[1] >= 0) {
+    // release the slot; the returned value is consumed so the atomic has
+    // completed before this CTA exits and the SM takes the next one
+    const unsigned r = atomicAnd(g_sm_slots + (slot_smem[2] & (kMaxSms - 1)), ~(1u << slot_smem[1]));
+    asm volatile("" ::"r"(r));
   }
 #ifdef SPARGE_CTA_TIMING
   if (threadIdx.x == 0) CTA_REC(3, gtimer());

@@ -24,6 +24,8 @@ n = bf.shape.B * bf.shape.Hq * ((bf.shape.N + 127) // 128)
 rec = np.zeros((1 << 16, 6), np.uint64)
 assert lib.sparge_debug_cta_records(rec.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(rec.nbytes)) == 0
 r = rec[:n].astype(np.int64)
+if os.environ.get("CTA_DUMP"):
+    np.save(os.environ["CTA_DUMP"], r)
 t0 = r[:, 0].min()
 entry, lstart, lend, exit_, sm, nt = (r[:, i] for i in range(6))
 span = exit_.max() - t0
