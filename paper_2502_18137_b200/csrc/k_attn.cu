@@ -338,7 +338,14 @@ __device__ __forceinline__ void exps64(const int32_t* a, float c, float m_ref, u
 }
 
 template <int D, bool CAUSAL, bool F16, bool QK16, bool PV8>
+// SPARGE_ATTN_MAXNREG=R (A/B option): cap the 6-warp kernel at R registers
+// per thread instead of the launch bound's 170; at R <= 128 two CTAs fit an
+// SM in any warp placement (no refill gaps, see SPARGE_ATTN_8W above)
+#if defined(SPARGE_ATTN_MAXNREG) && !SPARGE_ATTN_8W
+__global__ void __maxnreg__(SPARGE_ATTN_MAXNREG)
+#else
 __global__ void __launch_bounds__(THREADS, 2)
+#endif
 k_sparse_attn(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
   using L = Smem<D, QK16, PV8>;
